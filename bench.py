@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark: single-index contraction throughput on B200 (BASELINE.json configs[1]).
+
+A step is the sweep of all 36 second-order x third-order single-index
+contraction cases (flat GEMM / strided batched / exceptional) at extent n
+(default n=256, fp32 via 3xTF32 tensor cores), each planned by the reference's
+dispatcher semantics and executed as one launch of the sm_100a library.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 256] [--dtype f32|f64]
+    python bench.py --impl reference ...   # the reference algorithm on the host CPU
+
+Weak scaling: every rank runs the full per-GPU sweep on its own operands (the
+batch/free-mode shard of a problem N times larger); there is no data-path
+collective.  value = FLOPs of all ranks / max-over-ranks device time.
+Inputs: 3 rotating operand sets per step, each larger than L2 at n >= 256, so
+consecutive cases never hit L2 for their operands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "contraction GFLOP/s and % roofline vs n (1/2/4/8 B200) next to CPU ref"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+FP64_NOMINAL_TFLOPS = 37.0  # HGX B200 datasheet FP64 / FP64 tensor core
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured"
+        return d
+    return dict(FALLBACK_PEAKS)
+
+
+def case_shapes(n):
+    from paper_1606_05696_b200.planner import enumerate_cases
+    out = []
+    for case in enumerate_cases(2, 3):
+        ext = dict(m=n, n=n, p=n, k=n)
+        out.append((case, ext))
+    return out
+
+
+def flops_bytes(n, itemsize):
+    """Algorithmic FLOPs and bytes of one case at extent n (beta = 0): A is
+    n^2, B and C are n^3."""
+    return 2.0 * n ** 4, itemsize * (n * n + 2.0 * n ** 3)
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def build_sets(cases, n, dtype, device, nsets, seed):
+    import torch
+    from paper_1606_05696_b200.layout import DenseTensor, Layout
+    from paper_1606_05696_b200.planner import plan_single_mode
+    g = torch.Generator(device=device).manual_seed(seed)
+    size_a, size_b = n * n, n ** 3
+    sets = []
+    for s in range(nsets):
+        a = (torch.rand(size_a, generator=g, device=device, dtype=dtype) * 2 - 1)
+        b = (torch.rand(size_b, generator=g, device=device, dtype=dtype) * 2 - 1)
+        c = torch.empty(size_b, device=device, dtype=dtype)
+        sets.append((a, b, c))
+    work = []
+    for i, (case, ext) in enumerate(cases):
+        spec_labels = (case.labels_a, case.labels_b, case.labels_c)
+        la = Layout.packed([ext[l] for l in case.labels_a])
+        lb = Layout.packed([ext[l] for l in case.labels_b])
+        lc = Layout.packed([ext[l] for l in case.labels_c])
+        from paper_1606_05696_b200.notation import ContractionSpec
+        plan = plan_single_mode(ContractionSpec(*spec_labels), la, lb, lc)
+        a, b, c = sets[i % nsets]
+        # the order-2 operand may be A or B of the case: bind buffers by size
+        ta = DenseTensor(la, a if la.size == size_a else b)
+        tb = DenseTensor(lb, a if lb.size == size_a else b)
+        work.append((case.case_id, plan, ta, tb, DenseTensor(lc, c)))
+    return work
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1606_05696_b200 import _lib
+    from paper_1606_05696_b200.planner import execute_plan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(device)
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    itemsize = 4 if dtype == torch.float32 else 8
+    n = args.n
+    cases = case_shapes(n)
+    work = build_sets(cases, n, dtype, device, 3, seed=1234 + rank)
+    stream = torch.cuda.current_stream(device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[device.index])
+
+    nc = len(work)
+    kernel_of = {}
+    for cid, plan, a, b, c in work:  # one untimed pass to learn kernel families
+        execute_plan(plan, a, b, 1.0, 0.0, c)
+        kernel_of[cid] = _lib.last_kernel()
+    for _ in range(args.warmup):
+        for cid, plan, a, b, c in work:
+            execute_plan(plan, a, b, 1.0, 0.0, c)
+    # events: one per case boundary per step, all on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nc + 1)]
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(device.index) as clocks:
+        for s in range(args.steps):
+            ev[s][0].record(stream)
+            for i, (cid, plan, a, b, c) in enumerate(work):
+                execute_plan(plan, a, b, 1.0, 0.0, c)
+                ev[s][i + 1].record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    barrier()
+    total_ms = ev[0][0].elapsed_time(ev[-1][nc])
+    per_case = [[ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps)]
+                for i in range(nc)]
+    kern_ms = total_ms
+    t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+
+    fl, by = flops_bytes(n, itemsize)
+    step_flops = fl * nc
+    value = step_flops * world / (ms_per_step * 1e-3) / 1e9
+
+    peaks = load_peaks()
+    if dtype == torch.float32:
+        peak_tflops = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]) / 2.0 / 3.0
+        peak_note = (f"3xTF32 = bf16_tflops({peaks['source']})/2/3; "
+                     f"fp32 SIMT nominal 74.4 TFLOP/s")
+    else:
+        peak_tflops = FP64_NOMINAL_TFLOPS
+        peak_note = "fp64 DMMA nominal (datasheet 37 TFLOP/s)"
+    hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    roof_ms = max(fl / (peak_tflops * 1e12), by / (hbm * 1e9)) * 1e3 * nc
+    # dominant kernel family
+    fam_ms, fam_flops = {}, {}
+    for i, (cid, *_r) in enumerate(work):
+        k = kernel_of[cid]
+        fam_ms[k] = fam_ms.get(k, 0.0) + statistics.mean(per_case[i])
+        fam_flops[k] = fam_flops.get(k, 0.0) + fl
+    dom = max(fam_ms, key=fam_ms.get)
+    dom_tflops = fam_flops[dom] / (fam_ms[dom] * 1e-3) / 1e12
+    bound = "tensor" if fl / by > (peak_tflops * 1e12) / (hbm * 1e9) else "hbm"
+    roofline = {
+        "bound": bound, "kernel": dom, "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+        "achieved": round(dom_tflops, 3) if bound == "tensor" else None,
+        "peak": round(peak_tflops, 2) if bound == "tensor" else hbm,
+        "frac": round(dom_tflops / peak_tflops, 4) if bound == "tensor" else None,
+        "traffic": None, "peak_source": peak_note,
+        "step_frac_of_roofline": round(roof_ms / ms_per_step, 4),
+        "kernel_share_of_step": round(fam_ms[dom] / (kern_ms / args.steps), 4),
+    }
+    per_case_out = {work[i][0]: {"ms": round(statistics.median(per_case[i]), 4),
+                                 "kernel": kernel_of[work[i][0]],
+                                 "tflops": round(fl / (statistics.median(per_case[i]) * 1e-3)
+                                                 / 1e12, 2)}
+                    for i in range(nc)}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, work, device, dtype, itemsize, n, step_flops, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(n, args)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32(3xTF32)" if dtype == torch.float32 else "f64",
+            "data": "synthetic U[-1,1] operands, packed column-major",
+            "config": {"workload": f"36-case single-index sweep (configs[1]) at n={n}",
+                       "n": n, "cases": nc, "gflop_per_step_per_gpu": round(step_flops / 1e9, 2),
+                       "parallelism": f"batch-sharded x{world} (no collective)",
+                       "l2": "3 rotating operand sets, each > L2 (126 MB) at n>=256",
+                       "alpha": 1.0, "beta": 0.0},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "wall_ms_timed_region": round(total_ms, 3),
+            "per_case": per_case_out,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, work, device, dtype, itemsize, n, step_flops, world):
+    """Same sweep through the public API with host buffers: per case, copy A and
+    B from pinned host memory, execute_plan, copy C back; all inside the timed
+    region (one sync per step)."""
+    import torch
+    from paper_1606_05696_b200.layout import DenseTensor
+    from paper_1606_05696_b200.planner import execute_plan
+    size_a, size_b = n * n, n ** 3
+    ha = torch.empty(size_a, dtype=dtype).uniform_(-1, 1).pin_memory()
+    hb = torch.empty(size_b, dtype=dtype).uniform_(-1, 1).pin_memory()
+    hc = torch.empty(size_b, dtype=dtype).pin_memory()
+    da = torch.empty(size_a, dtype=dtype, device=device)
+    db = torch.empty(size_b, dtype=dtype, device=device)
+    dc = torch.empty(size_b, dtype=dtype, device=device)
+    jobs = []
+    for cid, plan, a, b, c in work:
+        ta = DenseTensor(a.layout, da if a.layout.size == size_a else db)
+        tb = DenseTensor(b.layout, da if b.layout.size == size_a else db)
+        jobs.append((plan, ta, tb, DenseTensor(c.layout, dc)))
+
+    def step():
+        for plan, ta, tb, tc in jobs:
+            da.copy_(ha, non_blocking=True)
+            db.copy_(hb, non_blocking=True)
+            execute_plan(plan, ta, tb, 1.0, 0.0, tc)
+            hc.copy_(dc, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    h2d = len(jobs) * itemsize * (size_a + size_b)
+    d2h = len(jobs) * itemsize * size_b
+    return {"value": round(step_flops * world / dt / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 3), "steps": steps,
+            "api": "paper_1606_05696_b200.execute_plan with pinned host<->device copies"}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+# bounded per-step sample for --impl reference: one case of every dispatch class
+REFERENCE_SAMPLE = ("1.1", "1.3", "2.4", "3.4", "5.5", "6.4")
+
+
+def cpu_sample(n, dtype_name, only=None):
+    """The reference algorithm (oracle port: planner lowering + numpy/OpenBLAS
+    cores, fp64 arithmetic as the reference) on the same 36-case sweep."""
+    from oracle import plan as oplan
+    from paper_1606_05696_b200.planner import enumerate_cases  # case catalogue only
+    rng = np.random.default_rng(0)
+    src_dtype = np.float32 if dtype_name == "f32" else np.float64
+    a = rng.uniform(-1, 1, n * n).astype(src_dtype).astype(np.float64)
+    b = rng.uniform(-1, 1, n ** 3).astype(src_dtype).astype(np.float64)
+    c = np.empty(n ** 3)
+    cases = [c for c in enumerate_cases(2, 3) if only is None or c.case_id in only]
+    t0 = time.perf_counter()
+    for case in cases:
+        ext = dict(m=n, n=n, p=n, k=n)
+        x = a if len(case.labels_a) == 2 else b
+        y = a if len(case.labels_b) == 2 else b
+        oplan.contract(case.labels_a, case.labels_b, case.labels_c, ext, x, y, 1.0, 0.0, c)
+    dt = time.perf_counter() - t0
+    return len(cases) * 2.0 * n ** 4 / dt / 1e9, dt, len(cases)
+
+
+def cpu_baseline(n, args):
+    cores = os.cpu_count() or 1
+    gflops, dt, ncases = cpu_sample(n, args.dtype)
+    return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+            "sample": f"all {ncases} cases at n={n}, fp64 arithmetic on "
+                      f"{'fp32-rounded ' if args.dtype == 'f32' else ''}inputs, "
+                      f"numpy/OpenBLAS ({dt:.1f} s)"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    n = args.n
+    cpu_sample(min(n, 64), args.dtype, REFERENCE_SAMPLE)  # warm-up (BLAS threads, caches)
+    times = []
+    ncases = 0
+    for _ in range(args.steps):
+        gflops, dt, ncases = cpu_sample(n, args.dtype, REFERENCE_SAMPLE)
+        times.append(dt)
+    ms = statistics.median(times) * 1e3
+    value = ncases * 2.0 * n ** 4 / (ms * 1e-3) / 1e9
+    out = {"metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic U[-1,1]",
+           "config": {"workload": f"36-case single-index sweep (configs[1]) at n={n}", "n": n,
+                      "cases_timed_per_step": ncases},
+           "impl": "reference",
+           "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores,
+                            "kind": "port",
+                            "sample": f"{ncases} of the 36 cases ({', '.join(REFERENCE_SAMPLE)}) at "
+                                      f"n={n} per step (oracle port of the reference planner + "
+                                      "numpy/OpenBLAS cores, all host threads)"},
+           "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

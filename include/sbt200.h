@@ -1,0 +1,128 @@
+/*
+ * sbt200 -- C ABI of the B200 (sm_100a) extended-BLAS tensor-contraction library.
+ *
+ * This is the drop-in boundary for the reference's arithmetic seam
+ * (reference: /root/reference/pkg/src/sbtensor/backend.py:29-31), i.e. the
+ * functions every kernel entry point of kernels.py ends in.  At that seam the
+ * reference has already lowered op flags to element strides, so every entry
+ * point here is a fully strided (batched) GEMM over flat buffers:
+ *
+ *   C[oc + i*crs + j*ccs + p*cpt] = alpha * sum_l A[oa + i*ars + l*acs + p*apt]
+ *                                           * B[ob + l*brs + j*bcs + p*bpt]
+ *                                  + beta * C[...]         (C not read if beta == 0)
+ *
+ * Units: element (not byte) offsets and strides, int64, all >= 0 (a zero batch
+ * stride broadcasts that operand, reference test_kernels.py:84-96).
+ * Ownership: A and B are read, C is updated in place; the library allocates
+ * nothing on the device-pointer entry points.
+ * Errors: 0 on success, a negative SBT_E* code otherwise; sbt_last_error()
+ * returns a message for the calling thread.  The reference cores do no
+ * validation (validation lives in kernels.py); these entry points validate
+ * extents, strides and pointers so a bad call can never fault the device.
+ * Threading: re-entrant; work is enqueued on `stream` (a cudaStream_t, NULL =
+ * legacy default stream) and is complete after a stream synchronise.  The
+ * *_host variants take host buffers, copy in/out and synchronise before
+ * returning (the numpy-buffer seam of the reference).
+ */
+#ifndef SBT200_H
+#define SBT200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBT_OK 0
+#define SBT_EINVAL (-1)       /* bad extent / stride / pointer */
+#define SBT_EUNSUPPORTED (-2) /* no kernel for this request */
+#define SBT_ECUDA (-3)        /* CUDA runtime error (message in sbt_last_error) */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sbt_version(void);
+/* Message describing the last failure on the calling thread ("" if none). */
+const char* sbt_last_error(void);
+/* Number of device kernels this library has launched (process-wide). */
+int64_t sbt_launch_count(void);
+/* Name of the kernel family chosen for the most recent launch on this thread. */
+const char* sbt_last_kernel(void);
+/* Force a kernel family: 0 = auto, 1 = generic SIMT, 2 = tensor-core tiled,
+   3 = small-matrix batched.  Used by tests to cover every path. */
+int sbt_set_kernel_override(int which);
+
+/* ---- reference: _loops_numba.py:12-25 gemm_core (called by kernels.gemm, kernels.py:107) */
+int sbt_gemm_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* a, int64_t oa, int64_t ars, int64_t acs,
+                      const double* b, int64_t ob, int64_t brs, int64_t bcs,
+                      double beta, double* c, int64_t oc, int64_t crs, int64_t ccs,
+                      void* stream);
+int sbt_gemm_core_f32(int64_t m, int64_t n, int64_t k, float alpha,
+                      const float* a, int64_t oa, int64_t ars, int64_t acs,
+                      const float* b, int64_t ob, int64_t brs, int64_t bcs,
+                      float beta, float* c, int64_t oc, int64_t crs, int64_t ccs,
+                      void* stream);
+
+/* ---- reference: _loops_numba.py:28-35 batched_core (kernels.strided_batched_gemm,
+        kernels.py:156-176 via _run_batched :245-266) */
+int sbt_batched_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
+                         const double* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                         const double* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                         double beta, double* c, int64_t oc, int64_t crs, int64_t ccs,
+                         int64_t cpt, int64_t batch, void* stream);
+int sbt_batched_core_f32(int64_t m, int64_t n, int64_t k, float alpha,
+                         const float* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                         const float* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                         float beta, float* c, int64_t oc, int64_t crs, int64_t ccs,
+                         int64_t cpt, int64_t batch, void* stream);
+
+/* ---- reference: _loops_numba.py:38-68 ext_batched_core (kernels.strided_batched_gemm_ex,
+        kernels.py:207-225).  Same arithmetic; one operand has unit batch stride. */
+int sbt_ext_batched_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
+                             const double* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                             const double* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                             double beta, double* c, int64_t oc, int64_t crs, int64_t ccs,
+                             int64_t cpt, int64_t batch, void* stream);
+int sbt_ext_batched_core_f32(int64_t m, int64_t n, int64_t k, float alpha,
+                             const float* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                             const float* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                             float beta, float* c, int64_t oc, int64_t crs, int64_t ccs,
+                             int64_t cpt, int64_t batch, void* stream);
+
+/* ---- reference: planner.py:551-581 (LoopStep loop around one batched call).
+        Two nested batch modes in ONE launch: index p in [0,batch) uses the
+        *pt strides, q in [0,batch2) the *pt2 strides. */
+int sbt_batched2_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
+                          const double* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                          int64_t apt2,
+                          const double* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                          int64_t bpt2,
+                          double beta, double* c, int64_t oc, int64_t crs, int64_t ccs,
+                          int64_t cpt, int64_t cpt2, int64_t batch, int64_t batch2,
+                          void* stream);
+int sbt_batched2_core_f32(int64_t m, int64_t n, int64_t k, float alpha,
+                          const float* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                          int64_t apt2,
+                          const float* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                          int64_t bpt2,
+                          float beta, float* c, int64_t oc, int64_t crs, int64_t ccs,
+                          int64_t cpt, int64_t cpt2, int64_t batch, int64_t batch2,
+                          void* stream);
+
+/* ---- host-buffer seam: the reference's cores take flat numpy buffers
+        (backend.py:29-31).  These copy the touched span of A, B (and C) to the
+        device, run the same kernels, copy C back and synchronise. */
+int sbt_batched_core_host_f64(int64_t m, int64_t n, int64_t k, double alpha,
+                              const double* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                              const double* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                              double beta, double* c, int64_t oc, int64_t crs, int64_t ccs,
+                              int64_t cpt, int64_t batch);
+int sbt_batched_core_host_f32(int64_t m, int64_t n, int64_t k, float alpha,
+                              const float* a, int64_t oa, int64_t ars, int64_t acs, int64_t apt,
+                              const float* b, int64_t ob, int64_t brs, int64_t bcs, int64_t bpt,
+                              float beta, float* c, int64_t oc, int64_t crs, int64_t ccs,
+                              int64_t cpt, int64_t batch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBT200_H */

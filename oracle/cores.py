@@ -31,15 +31,21 @@ def _view(buf: np.ndarray, off: int, shape, strides, writeable=False):
 
 
 def _store(cv: np.ndarray, prod: np.ndarray, alpha: float, beta: float) -> None:
+    if alpha != 1.0:
+        prod *= alpha
     if beta == 0.0:
-        cv[...] = alpha * prod
+        cv[...] = prod
     else:
-        cv[...] = alpha * prod + beta * cv.astype(np.float64)
+        cv[...] = prod + beta * np.asarray(cv, dtype=np.float64)
+
+
+def _f64(v):
+    return np.asarray(v, dtype=np.float64)
 
 
 def gemm_core(m, n, k, alpha, a, oa, ars, acs, b, ob, brs, bcs, beta, c, oc, crs, ccs):
-    av = _view(a, oa, (m, k), (ars, acs)).astype(np.float64)
-    bv = _view(b, ob, (k, n), (brs, bcs)).astype(np.float64)
+    av = _f64(_view(a, oa, (m, k), (ars, acs)))
+    bv = _f64(_view(b, ob, (k, n), (brs, bcs)))
     cv = _view(c, oc, (m, n), (crs, ccs), writeable=True)
     _store(cv, av @ bv, float(alpha), float(beta))
 
@@ -48,8 +54,15 @@ def batched_core(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt,
                  beta, c, oc, crs, ccs, cpt, batch):
     if batch <= 0:
         return
-    av = _view(a, oa, (batch, m, k), (apt, ars, acs)).astype(np.float64)
-    bv = _view(b, ob, (batch, k, n), (bpt, brs, bcs)).astype(np.float64)
+    if m * n * k >= 32768:
+        # large matrices: the reference numpy backend's per-batch BLAS loop
+        # (_loops_numpy.py:32-38) is the fastest host form
+        for p in range(batch):
+            gemm_core(m, n, k, alpha, a, oa + p * apt, ars, acs, b, ob + p * bpt, brs, bcs,
+                      beta, c, oc + p * cpt, crs, ccs)
+        return
+    av = _f64(_view(a, oa, (batch, m, k), (apt, ars, acs)))
+    bv = _f64(_view(b, ob, (batch, k, n), (bpt, brs, bcs)))
     cv = _view(c, oc, (batch, m, n), (cpt, crs, ccs), writeable=True)
     _store(cv, np.matmul(av, bv), float(alpha), float(beta))
 

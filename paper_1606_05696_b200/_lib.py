@@ -1,0 +1,108 @@
+"""ctypes binding of libsbt200.so (the C ABI declared in include/sbt200.h).
+
+The library is the ONLY compute path: there is no CPU fallback.  Loading fails
+loudly when the shared object is missing or lacks a declared symbol.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from ctypes import c_double, c_float, c_int, c_int64, c_void_p
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libsbt200.so"
+
+SBT_OK = 0
+SBT_EINVAL = -1
+SBT_EUNSUPPORTED = -2
+SBT_ECUDA = -3
+
+_I = c_int64
+_P = c_void_p
+
+
+def _core_sig(real):
+    # m, n, k, alpha, a, oa, ars, acs, b, ob, brs, bcs, beta, c, oc, crs, ccs, stream
+    return [_I, _I, _I, real, _P, _I, _I, _I, _P, _I, _I, _I, real, _P, _I, _I, _I, _P]
+
+
+def _batched_sig(real, stream=True):
+    sig = [_I, _I, _I, real, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, real, _P, _I, _I, _I, _I, _I]
+    return sig + [_P] if stream else sig
+
+
+def _batched2_sig(real):
+    return [_I, _I, _I, real, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, real, _P, _I, _I,
+            _I, _I, _I, _I, _I, _P]
+
+
+# every symbol include/sbt200.h declares, with its ctypes signature
+SIGNATURES = {
+    "sbt_version": ([], c_int),
+    "sbt_last_error": ([], ctypes.c_char_p),
+    "sbt_launch_count": ([], c_int64),
+    "sbt_last_kernel": ([], ctypes.c_char_p),
+    "sbt_set_kernel_override": ([c_int], c_int),
+    "sbt_gemm_core_f64": (_core_sig(c_double), c_int),
+    "sbt_gemm_core_f32": (_core_sig(c_float), c_int),
+    "sbt_batched_core_f64": (_batched_sig(c_double), c_int),
+    "sbt_batched_core_f32": (_batched_sig(c_float), c_int),
+    "sbt_ext_batched_core_f64": (_batched_sig(c_double), c_int),
+    "sbt_ext_batched_core_f32": (_batched_sig(c_float), c_int),
+    "sbt_batched2_core_f64": (_batched2_sig(c_double), c_int),
+    "sbt_batched2_core_f32": (_batched2_sig(c_float), c_int),
+    "sbt_batched_core_host_f64": (_batched_sig(c_double, stream=False), c_int),
+    "sbt_batched_core_host_f32": (_batched_sig(c_float, stream=False), c_int),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load():
+    """Load (once) and return the CDLL with argtypes set."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise LibraryError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1606_05696_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError = missing export -> loud failure
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SBT_OK:
+        return
+    msg = load().sbt_last_error().decode(errors="replace")
+    if rc == SBT_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(load().sbt_launch_count())
+
+
+def last_kernel() -> str:
+    return load().sbt_last_kernel().decode()
+
+
+def set_kernel_override(which) -> None:
+    """0/'auto', 1/'generic', 2/'tensor', 3/'small'."""
+    names = {"auto": 0, "generic": 1, "tensor": 2, "small": 3}
+    which = names.get(which, which)
+    check(load().sbt_set_kernel_override(int(which)), "sbt_set_kernel_override")

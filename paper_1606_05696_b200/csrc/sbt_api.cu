@@ -1,0 +1,216 @@
+// C ABI of libsbt200 (declared in include/sbt200.h).
+//
+// Each extern "C" entry point replaces one function of the reference's
+// arithmetic seam (reference backend.py:29-31):
+//   sbt_gemm_core_*        <- _loops_numba.py:12-25  gemm_core
+//   sbt_batched_core_*     <- _loops_numba.py:28-35  batched_core
+//   sbt_ext_batched_core_* <- _loops_numba.py:38-68  ext_batched_core
+//   sbt_batched2_core_*    <- planner.py:551-581     LoopStep loop x batched_core
+//   sbt_batched_core_host_*  the same over host (numpy) buffers
+// The host side validates, picks a kernel family from the stride classes and
+// launches exactly one kernel on the caller's stream.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/sbt200.h"
+#include "sbt_common.cuh"
+#include "k_generic.cuh"
+#include "sbt_dispatch.cuh"
+
+namespace sbt {
+
+static std::atomic<int64_t> g_launches{0};
+static std::atomic<int> g_override{0};
+static thread_local std::string t_err;
+static thread_local const char* t_last_kernel = "";
+
+static int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+void note_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  t_last_kernel = name;
+}
+
+int kernel_override() { return g_override.load(std::memory_order_relaxed); }
+
+static int check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    return fail(SBT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  return SBT_OK;
+}
+
+template <typename T>
+static int validate(const GemmParams<T>& p) {
+  if (p.m < 1 || p.n < 1 || p.k < 1)
+    return fail(SBT_EINVAL, "extents must be positive (m, n, k >= 1)");
+  if (p.batch < 0 || p.batch2 < 0) return fail(SBT_EINVAL, "batch counts must be >= 0");
+  const int64_t s[] = {p.ars, p.acs, p.aps, p.aps2, p.brs, p.bcs,
+                       p.bps, p.bps2, p.crs, p.ccs, p.cps, p.cps2};
+  for (int64_t v : s)
+    if (v < 0) return fail(SBT_EINVAL, "strides must be non-negative");
+  if (!p.a || !p.b || !p.c) return fail(SBT_EINVAL, "null buffer pointer");
+  return SBT_OK;
+}
+
+template <typename T>
+static int run(GemmParams<T> p, cudaStream_t stream) {
+  int rc = validate(p);
+  if (rc != SBT_OK) return rc;
+  if (p.batch == 0 || p.batch2 == 0) return SBT_OK;  // reference: batch 0 is a no-op
+  rc = launch_gemm<T>(p, stream);
+  if (rc != SBT_OK) return rc;
+  return check_cuda(cudaGetLastError(), "kernel launch");
+}
+
+template <typename T>
+static GemmParams<T> make(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,
+                          int64_t ars, int64_t acs, int64_t apt, int64_t apt2, const T* b,
+                          int64_t ob, int64_t brs, int64_t bcs, int64_t bpt, int64_t bpt2, T beta,
+                          T* c, int64_t oc, int64_t crs, int64_t ccs, int64_t cpt, int64_t cpt2,
+                          int64_t batch, int64_t batch2) {
+  GemmParams<T> p;
+  p.m = m; p.n = n; p.k = k; p.batch = batch; p.batch2 = batch2;
+  p.a = a ? a + oa : nullptr; p.ars = ars; p.acs = acs; p.aps = apt; p.aps2 = apt2;
+  p.b = b ? b + ob : nullptr; p.brs = brs; p.bcs = bcs; p.bps = bpt; p.bps2 = bpt2;
+  p.c = c ? c + oc : nullptr; p.crs = crs; p.ccs = ccs; p.cps = cpt; p.cps2 = cpt2;
+  p.alpha = alpha; p.beta = beta;
+  if (oa < 0 || ob < 0 || oc < 0) { p.m = -1; }  // rejected by validate()
+  return p;
+}
+
+// ---- host-buffer path -------------------------------------------------------
+struct DeviceArena {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int device = -1;
+};
+static DeviceArena g_arena;
+
+static int64_t span_of(int64_t m, int64_t k, int64_t rs, int64_t cs, int64_t ps, int64_t batch) {
+  return 1 + (m - 1) * rs + (k - 1) * cs + (batch > 0 ? (batch - 1) * ps : 0);
+}
+
+template <typename T>
+static int run_host(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,
+                    int64_t ars, int64_t acs, int64_t apt, const T* b, int64_t ob, int64_t brs,
+                    int64_t bcs, int64_t bpt, T beta, T* c, int64_t oc, int64_t crs, int64_t ccs,
+                    int64_t cpt, int64_t batch) {
+  GemmParams<T> probe = make<T>(m, n, k, alpha, a, oa, ars, acs, apt, 0, b, ob, brs, bcs, bpt,
+                                0, beta, c, oc, crs, ccs, cpt, 0, batch, 1);
+  int rc = validate(probe);
+  if (rc != SBT_OK) return rc;
+  if (batch == 0) return SBT_OK;
+  const int64_t na = span_of(m, k, ars, acs, apt, batch);
+  const int64_t nb = span_of(k, n, brs, bcs, bpt, batch);
+  const int64_t nc = span_of(m, n, crs, ccs, cpt, batch);
+  const bool c_dense = (nc == m * n * batch);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t ba = align(na * sizeof(T)), bb = align(nb * sizeof(T)), bc = align(nc * sizeof(T));
+  std::lock_guard<std::mutex> lock(g_arena.mu);
+  int dev = 0;
+  if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) != SBT_OK) return rc;
+  if (g_arena.device != dev || g_arena.bytes < ba + bb + bc) {
+    if (g_arena.ptr) cudaFree(g_arena.ptr);
+    g_arena.ptr = nullptr;
+    g_arena.bytes = 0;
+    if ((rc = check_cuda(cudaMalloc(&g_arena.ptr, ba + bb + bc), "cudaMalloc")) != SBT_OK)
+      return rc;
+    g_arena.bytes = ba + bb + bc;
+    g_arena.device = dev;
+  }
+  char* base = static_cast<char*>(g_arena.ptr);
+  T* da = reinterpret_cast<T*>(base);
+  T* db = reinterpret_cast<T*>(base + ba);
+  T* dc = reinterpret_cast<T*>(base + ba + bb);
+  cudaStream_t s = 0;
+  if ((rc = check_cuda(cudaMemcpyAsync(da, a + oa, na * sizeof(T), cudaMemcpyHostToDevice, s),
+                       "H2D A")) != SBT_OK) return rc;
+  if ((rc = check_cuda(cudaMemcpyAsync(db, b + ob, nb * sizeof(T), cudaMemcpyHostToDevice, s),
+                       "H2D B")) != SBT_OK) return rc;
+  // C's span is copied in unless beta == 0 and the batch regions tile it exactly
+  // (otherwise the gaps between regions must survive the copy back).
+  if (beta != T(0) || !c_dense) {
+    if ((rc = check_cuda(cudaMemcpyAsync(dc, c + oc, nc * sizeof(T), cudaMemcpyHostToDevice, s),
+                         "H2D C")) != SBT_OK) return rc;
+  }
+  GemmParams<T> p = make<T>(m, n, k, alpha, da, 0, ars, acs, apt, 0, db, 0, brs, bcs, bpt, 0,
+                            beta, dc, 0, crs, ccs, cpt, 0, batch, 1);
+  if ((rc = run(p, s)) != SBT_OK) return rc;
+  if ((rc = check_cuda(cudaMemcpyAsync(c + oc, dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s),
+                       "D2H C")) != SBT_OK) return rc;
+  return check_cuda(cudaStreamSynchronize(s), "stream sync");
+}
+
+}  // namespace sbt
+
+using namespace sbt;
+
+extern "C" {
+
+int sbt_version(void) { return 100; }
+const char* sbt_last_error(void) { return t_err.c_str(); }
+int64_t sbt_launch_count(void) { return g_launches.load(); }
+const char* sbt_last_kernel(void) { return t_last_kernel; }
+int sbt_set_kernel_override(int which) {
+  if (which < 0 || which > 3) return SBT_EINVAL;
+  g_override.store(which);
+  return SBT_OK;
+}
+
+#define SBT_DEFINE(T, SUF)                                                                     \
+  int sbt_gemm_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,     \
+                          int64_t ars, int64_t acs, const T* b, int64_t ob, int64_t brs,        \
+                          int64_t bcs, T beta, T* c, int64_t oc, int64_t crs, int64_t ccs,      \
+                          void* stream) {                                                       \
+    return run(make<T>(m, n, k, alpha, a, oa, ars, acs, 0, 0, b, ob, brs, bcs, 0, 0, beta, c,   \
+                       oc, crs, ccs, 0, 0, 1, 1),                                               \
+               (cudaStream_t)stream);                                                           \
+  }                                                                                             \
+  int sbt_batched_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,  \
+                             int64_t ars, int64_t acs, int64_t apt, const T* b, int64_t ob,     \
+                             int64_t brs, int64_t bcs, int64_t bpt, T beta, T* c, int64_t oc,   \
+                             int64_t crs, int64_t ccs, int64_t cpt, int64_t batch,              \
+                             void* stream) {                                                    \
+    return run(make<T>(m, n, k, alpha, a, oa, ars, acs, apt, 0, b, ob, brs, bcs, bpt, 0, beta,  \
+                       c, oc, crs, ccs, cpt, 0, batch, 1),                                      \
+               (cudaStream_t)stream);                                                           \
+  }                                                                                             \
+  int sbt_ext_batched_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a,          \
+                                 int64_t oa, int64_t ars, int64_t acs, int64_t apt, const T* b, \
+                                 int64_t ob, int64_t brs, int64_t bcs, int64_t bpt, T beta,     \
+                                 T* c, int64_t oc, int64_t crs, int64_t ccs, int64_t cpt,       \
+                                 int64_t batch, void* stream) {                                 \
+    return run(make<T>(m, n, k, alpha, a, oa, ars, acs, apt, 0, b, ob, brs, bcs, bpt, 0, beta,  \
+                       c, oc, crs, ccs, cpt, 0, batch, 1),                                      \
+               (cudaStream_t)stream);                                                           \
+  }                                                                                             \
+  int sbt_batched2_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa, \
+                              int64_t ars, int64_t acs, int64_t apt, int64_t apt2, const T* b,  \
+                              int64_t ob, int64_t brs, int64_t bcs, int64_t bpt, int64_t bpt2,  \
+                              T beta, T* c, int64_t oc, int64_t crs, int64_t ccs, int64_t cpt,  \
+                              int64_t cpt2, int64_t batch, int64_t batch2, void* stream) {      \
+    return run(make<T>(m, n, k, alpha, a, oa, ars, acs, apt, apt2, b, ob, brs, bcs, bpt, bpt2,  \
+                       beta, c, oc, crs, ccs, cpt, cpt2, batch, batch2),                        \
+               (cudaStream_t)stream);                                                           \
+  }                                                                                             \
+  int sbt_batched_core_host_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a,         \
+                                  int64_t oa, int64_t ars, int64_t acs, int64_t apt,            \
+                                  const T* b, int64_t ob, int64_t brs, int64_t bcs,             \
+                                  int64_t bpt, T beta, T* c, int64_t oc, int64_t crs,           \
+                                  int64_t ccs, int64_t cpt, int64_t batch) {                    \
+    return run_host<T>(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta, c, oc, \
+                       crs, ccs, cpt, batch);                                                   \
+  }
+
+SBT_DEFINE(double, f64)
+SBT_DEFINE(float, f32)
+
+}  // extern "C"

@@ -1,0 +1,481 @@
+"""Single-mode contraction planning onto transpose-free strided batched GEMM.
+
+Planning semantics are the reference's (``planner.py:218-371``), so every
+case gets the same strategy, operand roles, op flags, batch mode and loop
+modes:
+
+1. extent-1 free modes are squeezed away;
+2. maximal runs of output modes that are contiguous and stride-mergeable in
+   both C and their owning operand are flattened into one GEMM mode;
+3. the operand owning C's first (unit-stride) mode provides the GEMM rows;
+   the other operand's GEMM column mode is its first stored mode when that is
+   free, else its largest free mode (ties -> later in C);
+4. if the first operand's unit-stride mode is neither C's first mode nor the
+   contracted one, the plan is the *extended* (exceptional) form, batched in
+   that unit-stride mode; otherwise the largest remaining free mode (ties ->
+   later in C) is the batch mode and any others become loop modes.
+
+Execution is where this build departs: ``execute_plan`` lowers the plan to
+ONE launch of the sm_100a library -- the batch mode and the innermost loop
+mode become the kernel's two grid batch dimensions (the reference runs a
+Python loop of batched calls, ``planner.py:551-581``) -- using the operands'
+actual element strides, so no operand is ever copied or permuted.
+"""
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+from math import factorial, prod
+
+from .kernels import KernelArgs, Op, core_call
+from .layout import DenseTensor, Layout
+from .notation import ContractionSpec, classify_indices
+
+
+class PlanError(ValueError):
+    pass
+
+
+class UnsupportedContractionError(PlanError):
+    """The single-mode planner requires exactly one contracted index."""
+
+
+class PlanConsistencyError(PlanError):
+    """Tensors passed to execute_plan do not match the planned layouts."""
+
+
+_FREE_LETTERS = "mnpqrstuvw"
+
+
+@dataclass(frozen=True)
+class Mode:
+    label: str
+    extent: int
+    stride: int
+
+
+@dataclass(frozen=True)
+class FlattenStep:
+    tensor: str
+    labels: tuple
+    merged: str
+
+
+@dataclass(frozen=True)
+class LoopStep:
+    label: str
+    extent: int
+
+
+@dataclass(frozen=True)
+class GemmStep:
+    first: str                  # tensor providing GEMM rows: "A" | "B"
+    op_first: Op
+    op_second: Op
+    m_label: object
+    n_label: object
+    k_label: str
+
+
+@dataclass(frozen=True)
+class BatchedStep:
+    gemm: GemmStep
+    batch_label: str
+    extent: int
+    extended: bool = False
+
+
+@dataclass
+class EvaluationPlan:
+    spec: ContractionSpec
+    layout_a: Layout
+    layout_b: Layout
+    layout_c: Layout
+    strategy: str
+    steps: list = field(default_factory=list)
+    predicted_transpositions: int = 0
+    eff: dict = field(default_factory=dict)
+    conventional: object = None
+    _launch: object = field(default=None, repr=False, compare=False)
+
+
+@dataclass(frozen=True)
+class CaseDescriptor:
+    case_id: str
+    labels_a: tuple
+    labels_b: tuple
+    labels_c: tuple
+    classification: str         # single-gemm | strided-batched | exceptional
+
+
+# ---------------------------------------------------------------------------
+# the 36-case (and general (a, b)-order) catalogue
+
+
+def _insert(seq, pos, item):
+    out = list(seq)
+    out.insert(pos, item)
+    return tuple(out)
+
+
+def enumerate_cases(order_a: int, order_b: int) -> list:
+    """Every single-mode contraction pattern of an order-a by order-b pair with
+    C fixed as the free labels in order; (a+b-2)! * a * b cases.  Case ids are
+    "<family>.<variant>": families enumerate A's free labels (permutations) and
+    k's position in A from the back; variants enumerate k's position in B then
+    B's free-label permutations (reference planner.py:132-167)."""
+    if order_a < 1 or order_b < 1:
+        raise ValueError("orders must be >= 1")
+    n_free = order_a + order_b - 2
+    if n_free > len(_FREE_LETTERS):
+        raise ValueError("orders too large to label")
+    free = tuple(_FREE_LETTERS[:n_free])
+    families = [(a_free, kpos) for a_free in itertools.permutations(free, order_a - 1)
+                for kpos in reversed(range(order_a))]
+    cases = []
+    for fam, (a_free, kpos_a) in enumerate(families, start=1):
+        labels_a = _insert(a_free, kpos_a, "k")
+        others = [l for l in free if l not in a_free]
+        variants = [_insert(b_free, kpos_b, "k") for kpos_b in range(order_b)
+                    for b_free in itertools.permutations(others)]
+        for var, labels_b in enumerate(variants, start=1):
+            spec = ContractionSpec(labels_a, labels_b, free)
+            cases.append(CaseDescriptor(f"{fam}.{var}", labels_a, labels_b, free,
+                                        _classify(spec)))
+    assert len(cases) == factorial(n_free) * order_a * order_b
+    return cases
+
+
+def find_case(order_a: int, order_b: int, case_id: str) -> CaseDescriptor:
+    for case in enumerate_cases(order_a, order_b):
+        if case.case_id == case_id:
+            return case
+    raise PlanError(f"no case {case_id} for orders ({order_a}, {order_b})")
+
+
+def _classify(spec: ContractionSpec) -> str:
+    """Structural class at packed layouts with distinct extents 3, 4, ... per
+    (sorted) label (reference planner.py:177-194)."""
+    labels = sorted(set(spec.labels_a) | set(spec.labels_b))
+    ext = {l: 3 + i for i, l in enumerate(labels)}
+    lay = [Layout.packed([ext[l] for l in labs] or [1])
+           for labs in (spec.labels_a, spec.labels_b, spec.labels_c)]
+    strategy = plan_single_mode(spec, *lay).strategy
+    return {"flattened-gemm": "single-gemm",
+            "extended-batched": "exceptional"}.get(strategy, "strided-batched")
+
+
+def classify_case(case: CaseDescriptor) -> str:
+    return case.classification
+
+
+# ---------------------------------------------------------------------------
+# planning
+
+
+class _ModeList(list):
+    def index_of(self, label):
+        for i, md in enumerate(self):
+            if md.label == label:
+                return i
+        return -1
+
+    def stride(self, label):
+        i = self.index_of(label)
+        return None if i < 0 else self[i].stride
+
+
+def _modes(labels, layout):
+    if len(labels) != layout.order:
+        raise PlanError(f"{len(labels)} labels for order-{layout.order} layout")
+    return _ModeList(Mode(l, d, s) for l, d, s in zip(labels, layout.dims, layout.strides))
+
+
+def _merge_runs(plan, tensors, owner):
+    """Greedy flattening of output runs (reference planner.py:252-285)."""
+    pos = 0
+    while pos < len(tensors["C"]) - 1:
+        out = tensors["C"]
+        who = owner[out[pos].label]
+        src = tensors[who]
+        end = pos
+        while end + 1 < len(out) and owner.get(out[end + 1].label) == who:
+            at = src.index_of(out[end].label)
+            nxt = out[end + 1]
+            if at < 0 or at + 1 >= len(src) or src[at + 1].label != nxt.label:
+                break
+            if nxt.stride != out[end].stride * out[end].extent:
+                break
+            if src[at + 1].stride != src[at].stride * src[at].extent:
+                break
+            end += 1
+        if end > pos:
+            run = tuple(md.label for md in out[pos:end + 1])
+            merged = "".join(run)
+            for t in (who, "C"):
+                lst = tensors[t]
+                at = lst.index_of(run[0])
+                group = lst[at:at + len(run)]
+                lst[at:at + len(run)] = [Mode(merged, prod(g.extent for g in group),
+                                              group[0].stride)]
+                plan.steps.append(FlattenStep(t, run, merged))
+            owner[merged] = who
+        pos += 1
+
+
+def plan_single_mode(spec: ContractionSpec, layout_a: Layout, layout_b: Layout,
+                     layout_c: Layout) -> EvaluationPlan:
+    contracted = classify_indices(spec).contracted
+    if len(contracted) != 1:
+        raise UnsupportedContractionError(
+            f"single-mode planner requires exactly one contracted index, got {contracted}")
+    k = contracted[0]
+    A = _modes(spec.labels_a, layout_a)
+    B = _modes(spec.labels_b, layout_b)
+    if spec.labels_c:
+        C = _modes(spec.labels_c, layout_c)
+    else:
+        if layout_c.dims != (1,):
+            raise PlanError("scalar output requires a single-element layout")
+        C = _ModeList()
+    extent = {md.label: md.extent for md in (*A, *B)}
+    for md in C:
+        if extent.get(md.label) != md.extent:
+            raise PlanError(f"extent mismatch for output label {md.label!r}")
+    if A[A.index_of(k)].extent != B[B.index_of(k)].extent:
+        raise PlanError(f"extent mismatch for contracted label {k!r}")
+
+    plan = EvaluationPlan(spec=spec, layout_a=layout_a, layout_b=layout_b,
+                          layout_c=layout_c, strategy="", steps=[])
+    keep = lambda md: md.label == k or md.extent > 1  # noqa: E731
+    tensors = {"A": _ModeList(filter(keep, A)), "B": _ModeList(filter(keep, B)),
+               "C": _ModeList(md for md in C if md.extent > 1)}
+    owner = {md.label: "A" for md in tensors["A"]}
+    owner.update({md.label: "B" for md in tensors["B"] if md.label != k})
+    _merge_runs(plan, tensors, owner)
+    A, B, C = tensors["A"], tensors["B"], tensors["C"]
+    plan.eff = {"A": tuple(A), "B": tuple(B), "C": tuple(C)}
+
+    if not C:
+        plan.steps.append(GemmStep("A", Op.Normal, Op.Normal, None, None, k))
+        plan.strategy = "flattened-gemm"
+        return plan
+    if C[0].stride != 1:
+        raise PlanError("output's leading free mode must have unit stride")
+    c1 = C[0].label
+    first = "A" if A.index_of(c1) >= 0 else "B"
+    X, Y = (A, B) if first == "A" else (B, A)
+    c_rank = lambda md: C.index_of(md.label)  # noqa: E731
+    free_x = [md for md in X if md.label not in (c1, k)]
+    free_y = [md for md in Y if md.label != k]
+    n_mode = None
+    if free_y:
+        n_mode = Y[0] if Y[0].label != k else max(free_y, key=lambda md: (md.extent, c_rank(md)))
+    op_second = Op.Normal if (n_mode is None or Y[0].label == k) else Op.Transpose
+    rest = free_x + [md for md in free_y if n_mode is None or md.label != n_mode.label]
+    n_label = n_mode.label if n_mode else None
+
+    if X[0].label not in (c1, k):
+        batch = X[0]
+        rest = [md for md in rest if md.label != batch.label]
+        op_first = (Op.ExtendedNormal if X.index_of(c1) < X.index_of(k)
+                    else Op.ExtendedTranspose)
+        for md in sorted(rest, key=c_rank):
+            plan.steps.append(LoopStep(md.label, md.extent))
+        plan.steps.append(BatchedStep(GemmStep(first, op_first, op_second, c1, n_label, k),
+                                      batch.label, batch.extent, extended=True))
+        plan.strategy = "extended-batched"
+        return plan
+
+    op_first = Op.Normal if X[0].label == c1 else Op.Transpose
+    gemm = GemmStep(first, op_first, op_second, c1, n_label, k)
+    if not rest:
+        plan.steps.append(gemm)
+        plan.strategy = "flattened-gemm"
+        return plan
+    batch = max(rest, key=lambda md: (md.extent, c_rank(md)))
+    loops = sorted((md for md in rest if md.label != batch.label), key=c_rank)
+    for md in loops:
+        plan.steps.append(LoopStep(md.label, md.extent))
+    plan.steps.append(BatchedStep(gemm, batch.label, batch.extent))
+    plan.strategy = "nested-batched" if loops else "strided-batched"
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# lowering and execution
+
+
+@dataclass(frozen=True)
+class Launch:
+    """One library launch (plus the outer loop combos for plans with more than
+    one loop mode) with element strides taken from the planned layouts."""
+
+    first: str
+    m: int
+    n: int
+    k: int
+    strides: tuple              # (ars, acs, apt, apt2, brs, bcs, bpt, bpt2, crs, ccs, cpt, cpt2)
+    batch: int
+    batch2: int
+    outer: tuple                # ((x_off, y_off, c_off), ...) for loops beyond the fused one
+    extended: bool
+    kind: str
+
+
+def _gemm_and_batch(plan):
+    last = plan.steps[-1] if plan.steps else None
+    if isinstance(last, BatchedStep):
+        return last.gemm, last
+    if isinstance(last, GemmStep):
+        return last, None
+    raise PlanError(f"plan strategy {plan.strategy!r} has no GEMM step")
+
+
+def lower_plan(plan: EvaluationPlan) -> Launch:
+    if plan._launch is not None:
+        return plan._launch
+    gemm, batch = _gemm_and_batch(plan)
+    eff = {t: _ModeList(plan.eff[t]) for t in "ABC"}
+    X, Y = (eff["A"], eff["B"]) if gemm.first == "A" else (eff["B"], eff["A"])
+    C = eff["C"]
+    ext = {md.label: md.extent for md in (*eff["A"], *eff["B"], *C)}
+
+    def st(lst, label):
+        return (lst.stride(label) or 0) if label is not None else 0
+
+    m = ext[gemm.m_label] if gemm.m_label else 1
+    n = ext[gemm.n_label] if gemm.n_label else 1
+    k = ext[gemm.k_label]
+    ars, acs = st(X, gemm.m_label), st(X, gemm.k_label)
+    brs, bcs = st(Y, gemm.k_label), st(Y, gemm.n_label)
+    crs, ccs = st(C, gemm.m_label), st(C, gemm.n_label)
+    nb, apt, bpt, cpt = 1, 0, 0, 0
+    if batch is not None:
+        nb = batch.extent
+        apt, bpt, cpt = st(X, batch.batch_label), st(Y, batch.batch_label), st(C, batch.batch_label)
+    loops = [s for s in plan.steps if isinstance(s, LoopStep)]
+    nb2, apt2, bpt2, cpt2 = 1, 0, 0, 0
+    if loops:
+        inner = loops[-1]
+        nb2 = inner.extent
+        apt2, bpt2, cpt2 = st(X, inner.label), st(Y, inner.label), st(C, inner.label)
+    outer = []
+    for combo in itertools.product(*(range(s.extent) for s in loops[:-1])):
+        offs = [0, 0, 0]
+        for s, idx in zip(loops[:-1], combo):
+            for t, lst in enumerate((X, Y, C)):
+                offs[t] += idx * st(lst, s.label)
+        outer.append(tuple(offs))
+    kind = ("gemm" if batch is None else
+            "strided_batched_gemm_ex" if batch.extended else "strided_batched_gemm")
+    plan._launch = Launch(gemm.first, m, n, k,
+                          (ars, acs, apt, apt2, brs, bcs, bpt, bpt2, crs, ccs, cpt, cpt2),
+                          nb, nb2, tuple(outer) or ((0, 0, 0),),
+                          bool(batch is not None and batch.extended), kind)
+    return plan._launch
+
+
+def _storage_overlap(x, y) -> bool:
+    if x.device != y.device:
+        return False
+    xs, ys = x.data_ptr(), y.data_ptr()
+    xe, ye = xs + x.numel() * x.element_size(), ys + y.numel() * y.element_size()
+    return xs < ye and ys < xe
+
+
+def _check_tensor(planned: Layout, t: DenseTensor, name: str):
+    if t.layout != planned:
+        raise PlanConsistencyError(
+            f"layout of {name} drifted from the planned layout: {t.layout} != {planned}")
+
+
+def execute_plan(plan: EvaluationPlan, a: DenseTensor, b: DenseTensor,
+                 alpha: float, beta: float, c: DenseTensor,
+                 threads: int = 1, counters=None) -> None:
+    """Run a plan on device tensors, mutating C in place (one kernel launch
+    per plan for every case with at most one loop mode)."""
+    _check_tensor(plan.layout_a, a, "A")
+    _check_tensor(plan.layout_b, b, "B")
+    _check_tensor(plan.layout_c, c, "C")
+    if _storage_overlap(c.data, a.data) or _storage_overlap(c.data, b.data):
+        raise PlanError("C must not alias A or B")
+    if plan.strategy not in ("flattened-gemm", "strided-batched", "nested-batched",
+                             "extended-batched"):
+        raise PlanError(f"strategy {plan.strategy!r} is not executed by this backend")
+    L = lower_plan(plan)
+    x, y = (a.data, b.data) if L.first == "A" else (b.data, a.data)
+    ars, acs, apt, apt2, brs, bcs, bpt, bpt2, crs, ccs, cpt, cpt2 = L.strides
+    for ox, oy, oc in L.outer:
+        core_call(L.m, L.n, L.k, alpha, x, ox, ars, acs, apt, y, oy, brs, bcs, bpt, beta,
+                  c.data, oc, crs, ccs, cpt, batch=L.batch, apt2=apt2, bpt2=bpt2, cpt2=cpt2,
+                  batch2=L.batch2, extended=L.extended)
+        if counters is not None:
+            counters.kernel_calls[L.kind] = counters.kernel_calls.get(L.kind, 0) + 1
+
+
+# ---------------------------------------------------------------------------
+# reporting
+
+
+def _render_tensor(name, modes, batch_label=None):
+    body = []
+    for md in modes:
+        text = md.label if len(md.label) == 1 else f"({md.label})"
+        body.append(f"[{text}]" if md.label == batch_label else text)
+    return f"{name}[{''.join(body)}]"
+
+
+def render_plan(plan: EvaluationPlan) -> str:
+    """Paper-style notation, one step per line (reference planner.py:730-781)."""
+    gemm, batch = _gemm_and_batch(plan)
+    blabel = batch.batch_label if batch else None
+    lines, indent = [], ""
+    for step in plan.steps:
+        if isinstance(step, LoopStep):
+            lines.append(f"{indent}for {step.label} in [0,{step.extent}):")
+            indent += "  "
+    second = "B" if gemm.first == "A" else "A"
+    tf = "^T" if gemm.op_first in (Op.Transpose, Op.ExtendedTranspose) else ""
+    ts = "^T" if gemm.op_second is Op.Transpose else ""
+    lines.append(f"{indent}{_render_tensor('C', plan.eff['C'], blabel)} = "
+                 f"{_render_tensor(gemm.first, plan.eff[gemm.first], blabel)}{tf} "
+                 f"{_render_tensor(second, plan.eff[second], blabel)}{ts}")
+    return "\n".join(lines)
+
+
+def resolved_kernel_args(plan: EvaluationPlan, alpha=1.0, beta=0.0):
+    """The reference's KernelArgs for the plan's (batched) GEMM step
+    (planner.py:784-830): ld/lo in the op-flag convention of kernels.py."""
+    last = plan.steps[-1] if plan.steps else None
+    if not isinstance(last, (GemmStep, BatchedStep)):
+        return None
+    gemm, batch = _gemm_and_batch(plan)
+    eff = {t: _ModeList(plan.eff[t]) for t in "ABC"}
+    X, Y = (eff["A"], eff["B"]) if gemm.first == "A" else (eff["B"], eff["A"])
+    C = eff["C"]
+    ext = {md.label: md.extent for md in (*eff["A"], *eff["B"], *C)}
+    m = ext[gemm.m_label] if gemm.m_label else 1
+    n = ext[gemm.n_label] if gemm.n_label else 1
+    k = ext[gemm.k_label]
+    two = [md for md in X if md.label in (gemm.m_label, gemm.k_label)]
+    if gemm.op_first is Op.Normal:
+        lda = X.stride(gemm.k_label)
+    elif gemm.op_first is Op.Transpose:
+        lda = X.stride(gemm.m_label)
+    else:
+        lda = two[0].stride
+    if gemm.op_second is Op.Normal:
+        ldb = Y.stride(gemm.n_label) if gemm.n_label else k
+    else:
+        ldb = Y.stride(gemm.k_label)
+    ldc = (C.stride(gemm.n_label) if gemm.n_label else max(m, 1)) or max(m, 1)
+    loa = lob = loc = count = 0
+    if batch is not None:
+        count = batch.extent
+        loc = C.stride(batch.batch_label)
+        lob = Y.stride(batch.batch_label) or 0
+        loa = two[1].stride if batch.extended else (X.stride(batch.batch_label) or 0)
+    return KernelArgs(opa=gemm.op_first, opb=gemm.op_second, m=m, n=n, k=k,
+                      alpha=alpha, beta=beta, lda=lda or max(m, 1), loa=loa,
+                      ldb=ldb or k, lob=lob, ldc=ldc, loc=loc, batch_count=count)

@@ -1,0 +1,373 @@
+"""Parity of the sm_100a path against the reference (golden fixtures) and the
+CPU oracle.  Tolerances (north_star): max_rel_err <= 1e-12 for fp64, <= 1e-5
+for fp32 (fp32 results are checked against an fp64 oracle run on the same
+fp32 values)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1606_05696_b200 as sbt  # noqa: E402
+from paper_1606_05696_b200 import _lib, backend, kernels, layout as L  # noqa: E402
+from paper_1606_05696_b200.kernels import Op  # noqa: E402
+from paper_1606_05696_b200.layout import DenseTensor, Layout  # noqa: E402
+from paper_1606_05696_b200.notation import ContractionSpec  # noqa: E402
+from paper_1606_05696_b200.planner import (BatchedStep, enumerate_cases, execute_plan,  # noqa: E402
+                                           find_case, plan_single_mode)
+from oracle import api as oapi, naive, plan as oplan  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float64: 1e-12, torch.float32: 1e-5}
+EXCEPTIONAL = {"3.4", "3.6", "4.4", "4.6", "5.4", "5.6", "6.4", "6.6"}
+
+
+def dev(x, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+@pytest.fixture(autouse=True)
+def _auto_kernels():
+    _lib.set_kernel_override("auto")
+    yield
+    _lib.set_kernel_override("auto")
+
+
+def _packed(spec, ext):
+    return (Layout.packed([ext[l] for l in spec.labels_a]),
+            Layout.packed([ext[l] for l in spec.labels_b]),
+            Layout.packed([ext[l] for l in spec.labels_c] or [1]))
+
+
+# ------------------------------------------------------------------ golden fixtures
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_all_36_cases_match_reference_outputs(golden_contract, dtype):
+    index, arr = golden_contract
+    for rec in index["records"]:
+        key = rec["key"]
+        spec = ContractionSpec(tuple(rec["a"]), tuple(rec["b"]), tuple(rec["c"]))
+        la, lb, lc = _packed(spec, rec["ext"])
+        a = DenseTensor(la, dev(arr[key + "_a"], dtype))
+        b = DenseTensor(lb, dev(arr[key + "_b"], dtype))
+        c = DenseTensor(lc, dev(arr[key + "_c0"], dtype))
+        execute_plan(plan_single_mode(spec, la, lb, lc), a, b, rec["alpha"], rec["beta"], c)
+        if dtype == torch.float64:
+            want = arr[key + "_c"]
+        else:  # fp64 oracle on the fp32-rounded inputs
+            want = host(c.data) * 0
+            want[:] = host(dev(arr[key + "_c0"], dtype))
+            oplan.contract(rec["a"], rec["b"], rec["c"], rec["ext"],
+                           host(dev(arr[key + "_a"], dtype)), host(dev(arr[key + "_b"], dtype)),
+                           rec["alpha"], rec["beta"], want)
+        err = naive.max_rel_err(host(c.data), want)
+        assert err <= TOL[dtype], (key, err)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_kernel_entry_points_match_reference(golden_kernels, dtype):
+    index, arr = golden_kernels
+    for rec in index["records"]:
+        name, kw = rec["name"], dict(rec["kw"])
+        a, b = dev(arr[name + "_a"], dtype), dev(arr[name + "_b"], dtype)
+        c = dev(arr[name + "_c0"], dtype)
+        getattr(kernels, rec["fn"])(a=a, b=b, c=c, **kw)
+        if dtype == torch.float64:
+            want = arr[name + "_c"]
+        else:
+            want = host(dev(arr[name + "_c0"], dtype))
+            oapi.run_call(rec["fn"], kw, host(a), host(b), want)
+        assert naive.max_rel_err(host(c), want) <= TOL[dtype], name
+
+
+def test_numpy_buffers_take_the_host_seam(golden_kernels):
+    index, arr = golden_kernels
+    for rec in index["records"]:
+        name = rec["name"]
+        c = arr[name + "_c0"].copy()
+        getattr(kernels, rec["fn"])(a=arr[name + "_a"].copy(), b=arr[name + "_b"].copy(), c=c,
+                                    **rec["kw"])
+        assert naive.max_rel_err(c, arr[name + "_c"]) <= 1e-12, name
+
+
+def test_backend_adapter_reference_signatures(golden_kernels):
+    index, arr = golden_kernels
+    for rec in index["records"]:
+        name = rec["name"]
+        cl = oapi.lower_call(rec["fn"], rec["kw"])
+        c = arr[name + "_c0"].copy()
+        backend.batched_core(cl["m"], cl["n"], cl["k"], rec["kw"]["alpha"], arr[name + "_a"],
+                             cl["oa"], cl["ars"], cl["acs"], cl["apt"], arr[name + "_b"], cl["ob"],
+                             cl["brs"], cl["bcs"], cl["bpt"], rec["kw"]["beta"], c, cl["oc"],
+                             cl["crs"], cl["ccs"], cl["cpt"], cl["batch"])
+        assert naive.max_rel_err(c, arr[name + "_c"]) <= 1e-12, name
+
+
+def test_host_seam_preserves_gaps_in_c():
+    rng = np.random.default_rng(7)
+    m, n, k, P = 3, 4, 5, 6
+    a, b = rng.standard_normal(m * k * P), rng.standard_normal(k * n * P)
+    c = rng.standard_normal(2 * m * n * P)       # ldc = 2m: every other column is a gap
+    want = c.copy()
+    oapi.run_call("strided_batched_gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=1.0,
+                  lda=m, loa=m * k, ldb=k, lob=k * n, beta=0.0, ldc=2 * m, loc=2 * m * n,
+                  batch_count=P), a, b, want)
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.0, a, m, m * k, b, k, k * n, 0.0, c,
+                                 2 * m, 2 * m * n, P)
+    np.testing.assert_allclose(c, want, rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------------ reference semantics
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_beta_zero_ignores_nan(dtype):
+    c = torch.full((4,), float("nan"), dtype=dtype, device="cuda")
+    one = torch.ones(4, dtype=dtype, device="cuda")
+    kernels.gemm(Op.Normal, Op.Normal, 2, 2, 2, 1.0, one, 2, one, 2, 0.0, c, 2)
+    assert torch.equal(c.cpu(), torch.full((4,), 2.0, dtype=dtype))
+
+
+def test_batch_zero_and_broadcast():
+    c = torch.full((8,), 5.0, dtype=torch.float64, device="cuda")
+    z = torch.zeros(8, dtype=torch.float64, device="cuda")
+    n0 = _lib.launch_count()
+    kernels.strided_batched_gemm(Op.Normal, Op.Normal, 2, 2, 2, 1.0, z, 2, 4, z, 2, 4, 0.0, c,
+                                 2, 4, 0)
+    assert _lib.launch_count() == n0
+    assert torch.equal(c.cpu(), torch.full((8,), 5.0, dtype=torch.float64))
+    rng = np.random.default_rng(3)
+    m, n, k, P = 3, 4, 2, 5
+    A = rng.standard_normal((m, k, P))
+    B = rng.standard_normal((k, n))
+    c = torch.zeros(m * n * P, dtype=torch.float64, device="cuda")
+    kernels.strided_batched_gemm(Op.Normal, Op.Normal, m, n, k, 1.0,
+                                 dev(A.reshape(-1, order="F")), m, m * k,
+                                 dev(B.reshape(-1, order="F")), k, 0, 0.0, c, m, m * n, P)
+    want = np.einsum("ikp,kn->inp", A, B)
+    np.testing.assert_allclose(host(c).reshape((m, n, P), order="F"), want, atol=1e-13)
+
+
+def test_extended_equals_per_batch_loop():
+    rng = np.random.default_rng(4)
+    for exop in (Op.ExtendedNormal, Op.ExtendedTranspose):
+        m, n, k, P = 3, 4, 2, 5
+        a = dev(rng.standard_normal(P * m * k + 7))
+        b = dev(rng.standard_normal(max(k, n) ** 2 + 40))
+        lda, loa = (P, P * m) if exop is Op.ExtendedNormal else (P, P * k)
+        c1 = torch.zeros(m * n * P, dtype=torch.float64, device="cuda")
+        c2 = torch.zeros_like(c1)
+        args = (exop, Op.Normal, m, n, k, 1.0, a, lda, loa, b, k, 0, 0.0)
+        kernels.strided_batched_gemm_ex(*args, c1, m, m * n, P)
+        kernels.strided_batched_gemm_ex_reference(*args, c2, m, m * n, P)
+        assert naive.max_rel_err(host(c1), host(c2)) <= 1e-15
+
+
+def test_extended_matches_permute_then_batched():
+    rng = np.random.default_rng(3)
+    for cid in sorted(EXCEPTIONAL):
+        case = find_case(2, 3, cid)
+        spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+        ext = {l: int(rng.integers(2, 9)) for l in "mnpk"}
+        la, lb, lc = _packed(spec, ext)
+        A = rng.uniform(-1, 1, la.dims)
+        Bt = rng.uniform(-1, 1, lb.dims)
+        a, b = DenseTensor.from_array(A), DenseTensor.from_array(Bt)
+        c = DenseTensor.zeros(lc)
+        plan = plan_single_mode(spec, la, lb, lc)
+        step = plan.steps[-1]
+        assert isinstance(step, BatchedStep) and step.extended
+        execute_plan(plan, a, b, 1.0, 0.0, c)
+        first = step.gemm.first
+        labels_x = spec.labels_a if first == "A" else spec.labels_b
+        X = A if first == "A" else Bt
+        pos = labels_x.index(step.batch_label)
+        perm = [i for i in range(len(labels_x)) if i != pos] + [pos]
+        x2 = DenseTensor.from_array(np.transpose(X, perm))
+        lx2 = tuple(labels_x[i] for i in perm)
+        spec2 = (ContractionSpec(lx2, spec.labels_b, spec.labels_c) if first == "A"
+                 else ContractionSpec(spec.labels_a, lx2, spec.labels_c))
+        a2, b2 = (x2, b) if first == "A" else (a, x2)
+        c2 = DenseTensor.zeros(lc)
+        plan2 = plan_single_mode(spec2, a2.layout, b2.layout, c2.layout)
+        assert plan2.strategy != "extended-batched"
+        execute_plan(plan2, a2, b2, 1.0, 0.0, c2)
+        assert naive.max_rel_err(c.host_data(), c2.host_data()) <= 1e-13, cid
+
+
+def test_zero_copies_and_one_launch_per_plan():
+    rng = np.random.default_rng(2)
+    ext = dict(m=5, n=4, p=6, k=3)
+    for case in enumerate_cases(2, 3):
+        spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+        la, lb, lc = _packed(spec, ext)
+        a = DenseTensor.from_array(rng.uniform(-1, 1, la.dims))
+        b = DenseTensor.from_array(rng.uniform(-1, 1, lb.dims))
+        c = DenseTensor.zeros(lc)
+        plan = plan_single_mode(spec, la, lb, lc)
+        assert plan.predicted_transpositions == 0
+        t0, a0, n0 = L.transposition_count(), L.allocation_count(), _lib.launch_count()
+        torch.cuda.synchronize()
+        mem0 = torch.cuda.memory_allocated()
+        execute_plan(plan, a, b, 1.0, 0.0, c)
+        torch.cuda.synchronize()
+        assert (L.transposition_count(), L.allocation_count()) == (t0, a0), case.case_id
+        assert torch.cuda.memory_allocated() == mem0
+        assert _lib.launch_count() == n0 + 1, case.case_id
+
+
+def test_nested_batching_single_launch():
+    rng = np.random.default_rng(4)
+    spec = ContractionSpec(tuple("mkp"), tuple("nkq"), tuple("mnpq"))
+    for p, q in ((4, 7), (7, 4)):
+        ext = dict(m=5, n=6, k=3, p=p, q=q)
+        la, lb, lc = _packed(spec, ext)
+        A, B = rng.uniform(-1, 1, la.dims), rng.uniform(-1, 1, lb.dims)
+        a, b, c = DenseTensor.from_array(A), DenseTensor.from_array(B), DenseTensor.zeros(lc)
+        n0 = _lib.launch_count()
+        execute_plan(plan_single_mode(spec, la, lb, lc), a, b, 1.0, 0.0, c)
+        assert _lib.launch_count() == n0 + 1
+        want = np.einsum("mkp,nkq->mnpq", A, B)
+        assert naive.max_rel_err(c.to_array(), want) <= 1e-12
+
+
+def test_aliased_output_and_drift_rejected():
+    spec = sbt.parse_contraction("C[mn] = A[mk] * B[kn]")
+    a = DenseTensor.from_array(np.ones((3, 3)))
+    b = DenseTensor.from_array(np.ones((3, 3)))
+    c = DenseTensor.zeros((3, 3))
+    plan = plan_single_mode(spec, a.layout, b.layout, c.layout)
+    with pytest.raises(sbt.PlanError):
+        execute_plan(plan, a, b, 1.0, 0.0, DenseTensor(c.layout, a.data))
+    with pytest.raises(sbt.PlanError):
+        execute_plan(plan, a, b, 1.0, 0.0, DenseTensor.zeros((3, 4)))
+
+
+def test_scalar_output_dot():
+    rng = np.random.default_rng(5)
+    spec = ContractionSpec(("k",), ("k",), ())
+    x, y = rng.uniform(-1, 1, 7), rng.uniform(-1, 1, 7)
+    a, b = DenseTensor.from_array(x), DenseTensor.from_array(y)
+    c = DenseTensor.zeros((1,))
+    execute_plan(plan_single_mode(spec, a.layout, b.layout, c.layout), a, b, 2.0, 0.0, c)
+    assert abs(c.host_data()[0] - 2.0 * x @ y) <= 1e-13
+
+
+# ------------------------------------------------------------------ larger sizes vs oracle
+
+
+def _case_run(cid, n, dtype, seed, alpha=1.0, beta=0.0):
+    rng = np.random.default_rng(seed)
+    case = find_case(2, 3, cid)
+    spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+    ext = dict(m=n, n=n, p=n, k=n)
+    la, lb, lc = _packed(spec, ext)
+    ha = rng.uniform(-1, 1, la.size)
+    hb = rng.uniform(-1, 1, lb.size)
+    hc = rng.uniform(-1, 1, lc.size)
+    a = DenseTensor(la, dev(ha, dtype))
+    b = DenseTensor(lb, dev(hb, dtype))
+    c = DenseTensor(lc, dev(hc, dtype))
+    execute_plan(plan_single_mode(spec, la, lb, lc), a, b, alpha, beta, c)
+    want = host(dev(hc, dtype)).copy()
+    oplan.contract(spec.labels_a, spec.labels_b, spec.labels_c, ext, host(a.data),
+                   host(b.data), alpha, beta, want)
+    return naive.max_rel_err(host(c.data), want)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("n", [64, 128])
+def test_36_cases_square_vs_oracle(n, dtype):
+    for i, case in enumerate(enumerate_cases(2, 3)):
+        err = _case_run(case.case_id, n, dtype, seed=1000 * n + i, alpha=1.25,
+                        beta=0.5 if i % 3 == 0 else 0.0)
+        assert err <= TOL[dtype], (case.case_id, n, err)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("cid", ["1.1", "1.3", "2.4", "3.4", "5.5", "6.4", "6.6"])
+def test_selected_cases_n256_vs_oracle(cid, dtype):
+    err = _case_run(cid, 256, dtype, seed=hash(cid) % 1000)
+    assert err <= TOL[dtype], (cid, err)
+
+
+@pytest.mark.parametrize("which", ["generic", "auto"])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_kernel_families_agree_on_odd_and_aligned_shapes(which, dtype):
+    _lib.set_kernel_override(which)
+    rng = np.random.default_rng(11)
+    for (m, n, k, P) in ((7, 5, 3, 9), (33, 17, 65, 4), (128, 96, 64, 3), (256, 256, 128, 2)):
+        for opa in ("N", "T"):
+            for opb in ("N", "T"):
+                lda = m if opa == "N" else k
+                ldb = k if opb == "N" else n
+                ha, hb = rng.uniform(-1, 1, m * k * P), rng.uniform(-1, 1, k * n * P)
+                c = torch.zeros(m * n * P, dtype=dtype, device="cuda")
+                a, b = dev(ha, dtype), dev(hb, dtype)
+                kernels.strided_batched_gemm(opa, opb, m, n, k, 1.0, a, lda, m * k, b, ldb, k * n,
+                                             0.0, c, m, m * n, P)
+                want = np.zeros(m * n * P)
+                oapi.run_call("strided_batched_gemm", dict(opa=opa, opb=opb, m=m, n=n, k=k,
+                              alpha=1.0, lda=lda, loa=m * k, ldb=ldb, lob=k * n, beta=0.0,
+                              ldc=m, loc=m * n, batch_count=P), host(a), host(b), want)
+                assert naive.max_rel_err(host(c), want) <= TOL[dtype], (m, n, k, P, opa, opb)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+def test_small_matrix_batches(n, dtype):
+    rng = np.random.default_rng(n)
+    P = 2000
+    ha, hb = rng.uniform(-1, 1, n * n * P), rng.uniform(-1, 1, n * n * P)
+    a, b = dev(ha, dtype), dev(hb, dtype)
+    c = torch.zeros(n * n * P, dtype=dtype, device="cuda")
+    kernels.strided_batched_gemm("N", "N", n, n, n, 1.0, a, n, n * n, b, n, n * n, 0.0, c, n,
+                                 n * n, P)
+    want = np.matmul(host(a).reshape(P, n, n).transpose(0, 2, 1),
+                     host(b).reshape(P, n, n).transpose(0, 2, 1)).transpose(0, 2, 1).reshape(-1)
+    assert naive.max_rel_err(host(c), want) <= TOL[dtype]
+
+
+# ------------------------------------------------------------------ Tucker / HOOI
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_hooi_matches_reference_fp64(golden_hooi, idx):
+    index, arr = golden_hooi
+    rec = index["records"][idx]
+    name = rec["name"]
+    t = DenseTensor(Layout.packed(rec["dims"]), dev(arr[name + "_t"]))
+    model = sbt.hooi(t, rec["ranks"], max_iters=rec["max_iters"])
+    assert abs(model.iterations - rec["iterations"]) <= (
+        1 if rec["fit_history"][-1] > 0.999999 else 0)
+    nf = min(len(model.fit_history), len(rec["fit_history"]))
+    np.testing.assert_allclose(model.fit_history[:nf], rec["fit_history"][:nf], atol=1e-7)
+    for r in range(3):
+        u = model.factors[r].cpu().numpy()
+        ur = arr[f"{name}_u{r}"]
+        np.testing.assert_allclose(u @ u.T, ur @ ur.T, atol=1e-7)
+        np.testing.assert_allclose(u.T @ u, np.eye(u.shape[1]), atol=1e-10)
+    rec_t = sbt.tucker_reconstruct(model)
+    np.testing.assert_allclose(rec_t.host_data(), arr[name + "_rec"], atol=1e-7)
+
+
+def test_hooi_fp32_matches_oracle():
+    from oracle import tucker as otucker
+    rng = np.random.default_rng(9)
+    dims, ranks = (64, 48, 40), (6, 5, 4)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    t = DenseTensor.from_array(full, dtype="float32")
+    model = sbt.hooi(t, ranks, max_iters=4, tol=-1.0)
+    ref = otucker.hooi(t.to_array().astype(np.float64), ranks, max_iters=4, tol=-1.0)
+    np.testing.assert_allclose(model.fit_history, ref["fit_history"], rtol=1e-5)
+    for r in range(3):
+        u = model.factors[r].cpu().numpy()
+        ur = ref["factors"][r]
+        np.testing.assert_allclose(u @ u.T, ur @ ur.T, atol=1e-4)

@@ -2,12 +2,19 @@
 //
 // The reference picks its arithmetic core by entry point only
 // (kernels.py:107,174,223).  Here the same request is routed by stride class:
-//   K1/K2 tensor-core tiles  (aligned, unit-stride operands; TF32x3 / DMMA)
-//   K3    small-matrix batched (n <= 64, many batch entries)
-//   K4    generic SIMT       (anything else; always correct)
+//   tensor-core tiles (fp32: tcgen05 3xTF32; fp64: DMMA) when each operand has
+//       a unit-stride mode and 16-byte aligned other strides -- after
+//       orienting the problem (C^T = B^T A^T) so the larger extent is the
+//       128-row MMA dimension;
+//   small-matrix batched kernel for many tiny GEMMs;
+//   generic SIMT kernel for everything else (odd extents / strides).
 #pragma once
+#include <cstdlib>
+#include <utility>
+
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
+#include "k_tf32x3.cuh"
 
 namespace sbt {
 
@@ -36,8 +43,108 @@ static void launch_generic(const GemmParams<T>& p, cudaStream_t stream) {
   }
 }
 
+// C = A B  <=>  C^T = B^T A^T : swap operand roles and output strides.
+template <typename T>
+static GemmParams<T> transposed(const GemmParams<T>& p) {
+  GemmParams<T> q = p;
+  q.m = p.n; q.n = p.m;
+  q.a = p.b; q.ars = p.bcs; q.acs = p.brs; q.aps = p.bps; q.aps2 = p.bps2;
+  q.b = p.a; q.brs = p.acs; q.bcs = p.ars; q.bps = p.aps; q.bps2 = p.aps2;
+  q.crs = p.ccs; q.ccs = p.crs;
+  return q;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+static inline bool mult4(int64_t v) { return (v & 3) == 0; }
+static inline bool aligned16(const void* ptr) {
+  return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0;
+}
+
+// Operand major-ness for the 16-byte-vector tensor-core producers.
+// returns 1 = K-major, 2 = MN-major, 0 = not eligible
+template <typename T>
+static int a_major(const GemmParams<T>& p) {
+  if (!aligned16(p.a) || !mult4(p.aps) || !mult4(p.aps2)) return 0;
+  if (p.acs == 1 && mult4(p.ars) && mult4(p.k)) return 1;
+  if (p.ars == 1 && mult4(p.acs) && mult4(p.m)) return 2;
+  return 0;
+}
+template <typename T>
+static int b_major(const GemmParams<T>& p) {
+  if (!aligned16(p.b) || !mult4(p.bps) || !mult4(p.bps2)) return 0;
+  if (p.brs == 1 && mult4(p.bcs) && mult4(p.k)) return 1;
+  if (p.bcs == 1 && mult4(p.brs) && mult4(p.n)) return 2;
+  return 0;
+}
+
+template <int BN, bool AK, bool BK_>
+static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+  using C_ = tf32x3::Cfg<BN>;
+  auto kern = tf32x3::tf32x3_gemm_kernel<BN, AK, BK_>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C_::SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  const int64_t tiles_m = ceil_div(p.m, tf32x3::BM), tiles_n = ceil_div(p.n, BN);
+  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  if (total > int64_t(0x7fffffff)) return -2;
+  kern<<<dim3(unsigned(total)), dim3(tf32x3::kThreads), C_::SMEM_BYTES, stream>>>(
+      p, tiles_m, tiles_n);
+  note_launch("tc_tf32x3");
+  return 0;
+}
+
+template <int BN>
+static int launch_tf32x3_bn(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
+  if (am == 1 && bm == 1) return launch_tf32x3_cfg<BN, true, true>(p, s);
+  if (am == 1 && bm == 2) return launch_tf32x3_cfg<BN, true, false>(p, s);
+  if (am == 2 && bm == 1) return launch_tf32x3_cfg<BN, false, true>(p, s);
+  return launch_tf32x3_cfg<BN, false, false>(p, s);
+}
+
+// Returns 1 if launched, 0 if not eligible, <0 on error.
+static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
+  // orient: the larger of (m, n) becomes the 128-row MMA dimension
+  GemmParams<float> p = (p0.n > p0.m) ? transposed(p0) : p0;
+  int am = a_major(p), bm = b_major(p);
+  if (!am || !bm) {  // the other orientation may be eligible
+    GemmParams<float> q = transposed(p);
+    const int am2 = a_major(q), bm2 = b_major(q);
+    if (!am2 || !bm2) return 0;
+    p = q; am = am2; bm = bm2;
+  }
+  if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
+    return 0;
+  int bn = env_int("SBT_TC_BN", 0);
+  if (bn != 32 && bn != 64 && bn != 128 && bn != 256)
+    bn = p.n > 64 ? 128 : (p.n > 32 ? 64 : 32);
+  int rc;
+  switch (bn) {
+    case 256: rc = launch_tf32x3_bn<256>(p, am, bm, stream); break;
+    case 128: rc = launch_tf32x3_bn<128>(p, am, bm, stream); break;
+    case 64:  rc = launch_tf32x3_bn<64>(p, am, bm, stream); break;
+    default:  rc = launch_tf32x3_bn<32>(p, am, bm, stream); break;
+  }
+  return rc < 0 ? rc : 1;
+}
+
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
+  const int ov = kernel_override();
+  if constexpr (sizeof(T) == 4) {
+    if (ov == 0 || ov == 2) {
+      const int rc = try_tensor_f32(p, stream, ov == 2);
+      if (rc < 0) return rc;
+      if (rc == 1) return 0;
+    }
+  }
   launch_generic<T>(p, stream);
   return 0;
 }

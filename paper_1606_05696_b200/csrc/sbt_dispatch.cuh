@@ -15,6 +15,8 @@
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
 #include "k_tf32x3.cuh"
+#include "k_tf32x3_ts.cuh"
+#include "k_tf32x3_2cta.cuh"
 
 namespace sbt {
 
@@ -101,6 +103,44 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   return 0;
 }
 
+template <bool AK, bool BK_>
+static int launch_tf32ts_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+  auto kern = tf32ts::tf32x3_ts_kernel<AK, BK_>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tf32ts::SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  const int64_t tiles_m = ceil_div(p.m, tf32ts::BM), tiles_n = ceil_div(p.n, tf32ts::BN);
+  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  const int64_t grid = total < kNumSMs ? total : kNumSMs;
+  kern<<<dim3(unsigned(grid)), dim3(tf32ts::kThreads), tf32ts::SMEM_BYTES, stream>>>(
+      p, tiles_m, tiles_n, total);
+  note_launch("tc_tf32x3_ts");
+  return 0;
+}
+
+template <bool AK, bool BK_>
+static int launch_tf32pair_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+  auto kern = tf32pair::tf32x3_pair_kernel<AK, BK_>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tf32pair::SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  const int64_t tiles_m = ceil_div(p.m, tf32pair::BM), tiles_n = ceil_div(p.n, tf32pair::BN);
+  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
+  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32pair::kThreads), tf32pair::SMEM_BYTES, stream>>>(
+      p, tiles_m, tiles_n, total);
+  note_launch("tc_tf32x3_pair");
+  return 0;
+}
+
 template <int BN>
 static int launch_tf32x3_bn(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
   if (am == 1 && bm == 1) return launch_tf32x3_cfg<BN, true, true>(p, s);
@@ -122,9 +162,27 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
   }
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
+  // 0 auto, 1 = 1-CTA smem/smem tiles, 2 = A-in-TMEM persistent, 3 = CTA pair
+  static const int variant = env_int("SBT_TC_VARIANT", 0);
+  if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 3) {
+    int rc;
+    if (am == 1 && bm == 1) rc = launch_tf32pair_cfg<true, true>(p, stream);
+    else if (am == 1) rc = launch_tf32pair_cfg<true, false>(p, stream);
+    else if (bm == 1) rc = launch_tf32pair_cfg<false, true>(p, stream);
+    else rc = launch_tf32pair_cfg<false, false>(p, stream);
+    return rc < 0 ? rc : 1;
+  }
+  if (variant == 2 && p.n > 64) {
+    int rc;
+    if (am == 1 && bm == 1) rc = launch_tf32ts_cfg<true, true>(p, stream);
+    else if (am == 1) rc = launch_tf32ts_cfg<true, false>(p, stream);
+    else if (bm == 1) rc = launch_tf32ts_cfg<false, true>(p, stream);
+    else rc = launch_tf32ts_cfg<false, false>(p, stream);
+    return rc < 0 ? rc : 1;
+  }
   int bn = env_int("SBT_TC_BN", 0);
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256)
-    bn = p.n > 64 ? 128 : (p.n > 32 ? 64 : 32);
+    bn = p.n > 128 ? 256 : (p.n > 64 ? 128 : (p.n > 32 ? 64 : 32));
   int rc;
   switch (bn) {
     case 256: rc = launch_tf32x3_bn<256>(p, am, bm, stream); break;

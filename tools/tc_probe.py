@@ -43,3 +43,6 @@ if __name__ == "__main__":
         for opb in "NT":
             kern, err, t = run(opa, opb, 256, 256, 256, 256, reps=5)
             print(f"256^3 x256 {opa}{opb} {kern} err={err:.2e} {t:.3f} ms {2*256**4/t/1e9:.1f} TF/s", flush=True)
+    for (m, n, k, P) in ((2048, 2048, 2048, 4), (4096, 4096, 1024, 1)):
+        kern, err, t = run("N", "N", m, n, k, P, reps=5)
+        print(f"{m}x{n}x{k} x{P} NN {kern} err={err:.2e} {t:.3f} ms {2*m*n*k*P/t/1e9:.1f} TF/s", flush=True)

@@ -63,7 +63,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int mn4, int k, int mn_atoms) {
 
 template <int BN, bool A_K, bool B_K>
 __global__ void __launch_bounds__(kThreads, 1)
-tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
+tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n, int split_mode) {
   using C_ = Cfg<BN>;
   constexpr int STAGES = C_::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -145,10 +145,10 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
         const int e = tid + i * kProducers;
         const uint32_t off = A_K ? kmajor_off(e >> 3, e & 7) : mnmajor_off(e & 31, e >> 5, BM / 32);
         uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-        ptx::split_tf32(ra[i].x, h0, l0);
-        ptx::split_tf32(ra[i].y, h1, l1);
-        ptx::split_tf32(ra[i].z, h2, l2);
-        ptx::split_tf32(ra[i].w, h3, l3);
+        ptx::split_tf32_mode(ra[i].x, h0, l0, split_mode);
+        ptx::split_tf32_mode(ra[i].y, h1, l1, split_mode);
+        ptx::split_tf32_mode(ra[i].z, h2, l2, split_mode);
+        ptx::split_tf32_mode(ra[i].w, h3, l3, split_mode);
         ptx::sts_v4(a_hi + off, h0, h1, h2, h3);
         ptx::sts_v4(a_lo + off, l0, l1, l2, l3);
       }
@@ -158,10 +158,10 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
         const uint32_t off = B_K ? kmajor_off(e >> 3, e & 7)
                                  : mnmajor_off(e % (BN / 4), e / (BN / 4), BN / 32);
         uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-        ptx::split_tf32(rb[i].x, h0, l0);
-        ptx::split_tf32(rb[i].y, h1, l1);
-        ptx::split_tf32(rb[i].z, h2, l2);
-        ptx::split_tf32(rb[i].w, h3, l3);
+        ptx::split_tf32_mode(rb[i].x, h0, l0, split_mode);
+        ptx::split_tf32_mode(rb[i].y, h1, l1, split_mode);
+        ptx::split_tf32_mode(rb[i].z, h2, l2, split_mode);
+        ptx::split_tf32_mode(rb[i].w, h3, l3, split_mode);
         ptx::sts_v4(b_hi + off, h0, h1, h2, h3);
         ptx::sts_v4(b_lo + off, l0, l1, l2, l3);
       }

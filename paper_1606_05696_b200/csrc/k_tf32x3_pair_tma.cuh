@@ -1,0 +1,276 @@
+// K1 (fp32), production variant: 3xTF32 strided batched GEMM on
+// tcgen05.mma.cta_group::2 (UMMA 256 x 256), TMA-fed, persistent.
+//
+//   C = alpha * (A_hi B_hi + A_hi B_lo + A_lo B_hi) + beta * C
+//
+// The tensor core TRUNCATES fp32 operands to TF32 (measured: feeding the raw
+// fp32 tile as "hi" together with lo = x - trunc(x) reproduces the explicit
+// split to the last bit of accuracy, while lo = x - rna(x) does not).  So the
+// raw tile that TMA lands in shared memory IS the hi operand, and only the
+// residual lo = x - (x & ~0x1fff) has to be produced -- two ALU ops per
+// element, written at the same (swizzled) offset, so the converter never needs
+// to know the layout.
+//
+// Operand staging is in place at the operands' strides: a 4-D TMA tensor map
+// (contiguous mode, other mode, batch, batch2) per operand; K-major operands
+// use 128 B swizzle, MN-major ones 128 B swizzle with 32 B atoms (the only
+// MN-major layout UMMA accepts for tf32).  TMA zero-fills every M/N/K tail.
+//
+// CTA pair: each CTA holds its 128 rows of A and 128 of B's 256 columns; the
+// leader issues M=256 MMAs reading both CTAs' smem.  SPLIT_ACC keeps the two
+// small cross terms in a second TMEM accumulator: the tensor core truncates on
+// every accumulate, so folding 2^-11-sized terms into the main accumulator
+// would cost a full ulp(acc) each; with the split the error of K=1024 sums
+// drops ~3x.  (Two accumulators use all 512 TMEM columns, so SPLIT_ACC runs
+// with a single accumulator buffer; the default double-buffers instead.)
+//
+// Warp roles per CTA (14 warps): 0-3 epilogue, 4-11 lo converters,
+// 12 TMA producer + TMEM allocator, 13 MMA issuer (leader).
+#pragma once
+#include <cuda.h>
+
+#include "sbt_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace sbt {
+namespace tf32tma {
+
+constexpr int BM = 256, BN = 256, HM = 128, HN = 128, BK = 32;
+constexpr int STAGES = 3;
+constexpr int kThreads = 14 * 32;
+constexpr int kConvWarps = 8;
+constexpr int OP_BYTES = 128 * BK * 4;            // 16 KB: one operand half, raw or lo
+constexpr int STAGE_BYTES = 4 * OP_BYTES;          // A raw, A lo, B raw, B lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t kTxBytes = 2 * OP_BYTES;        // raw A + raw B per stage
+
+struct Tile {
+  int64_t m0, n0, pb, qb;
+};
+__device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tiles_n,
+                                        int64_t batch) {
+  Tile c;
+  c.m0 = (t % tiles_m) * BM;
+  t /= tiles_m;
+  c.n0 = (t % tiles_n) * BN;
+  t /= tiles_n;
+  c.pb = t % batch;
+  c.qb = t / batch;
+  return c;
+}
+
+// TMA loads of one operand half (128 rows/cols of the MMA dimension x 32 k).
+// K-major: one box (32 k, 128 mn).  MN-major: four boxes (32 mn, 32 k), one per
+// 32-wide MN atom column, each a contiguous 4 KB slab.
+template <bool KMAJ>
+__device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar,
+                                            int64_t mn0, int64_t k0, int64_t b, int64_t b2,
+                                            bool bcast, bool bcast2) {
+  const int cb = bcast ? 0 : int(b), cb2 = bcast2 ? 0 : int(b2);
+  if (KMAJ) {
+    ptx::tma_load_4d(dst, tm, bar, int(k0), int(mn0), cb, cb2);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      ptx::tma_load_4d(dst + c * 4096, tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
+  }
+}
+
+template <bool A_K, bool B_K, bool SPLIT_ACC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
+                       int64_t tiles_n, int64_t total) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = raw_full + STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const uint32_t rank = ptx::cluster_rank();
+  const int64_t pair = blockIdx.x >> 1;
+  const int64_t npairs = gridDim.x >> 1;
+  const int nkb = int((p.k + BK - 1) / BK);
+  constexpr int NBUF = SPLIT_ACC ? 1 : 2;
+
+  if (warp == 12) {
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        ptx::mbar_init(&raw_full[s], 1);
+        ptx::mbar_init(&full[s], 2 * kConvWarps);
+        ptx::mbar_init(&empty[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        ptx::mbar_init(&acc_full[b], 1);
+        ptx::mbar_init(&acc_empty[b], 2 * 128);
+      }
+      ptx::fence_mbarrier_init();
+      ptx::prefetch_tmap(&tmA);
+      ptx::prefetch_tmap(&tmB);
+    }
+    __syncwarp();
+    ptx::tmem_alloc2(tmem_slot, 512);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t my_tiles = (total - pair + npairs - 1) / npairs;
+  const int64_t n_iter = my_tiles * nkb;
+
+  if (warp == 12) {
+    if (lane == 0) {
+      // -------------------------------------------------------- TMA producer
+      const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
+      for (int64_t g = 0; g < n_iter; ++g) {
+        const uint32_t s = uint32_t(g % STAGES);
+        ptx::mbar_wait(&empty[s], (uint32_t(g / STAGES) & 1u) ^ 1u);
+        const Tile tc = tile_of(pair + (g / nkb) * npairs, tiles_m, tiles_n, p.batch);
+        const int64_t k0 = int64_t(g % nkb) * BK;
+        uint8_t* st = smem + s * STAGE_BYTES;
+        ptx::mbar_arrive_expect_tx(&raw_full[s], kTxBytes);
+        tma_operand<A_K>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc, a_bc2);
+        tma_operand<B_K>(&tmB, st + 2 * OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
+                         tc.qb, b_bc, b_bc2);
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + kConvWarps) {
+    // -------------------------------------------------------- lo converters
+    const int ct = tid - 128;  // 0..255
+    uint32_t full_leader[STAGES];
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) full_leader[s] = ptx::mapa(&full[s], 0);
+    for (int64_t g = 0; g < n_iter; ++g) {
+      const uint32_t s = uint32_t(g % STAGES);
+      ptx::mbar_wait(&raw_full[s], uint32_t(g / STAGES) & 1u);
+      const uint32_t base = ptx::smem_addr(smem + s * STAGE_BYTES);
+#pragma unroll
+      for (int op = 0; op < 2; ++op) {  // A then B
+        const uint32_t raw = base + op * 2 * OP_BYTES;
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = ptx::lds_v4(raw + (ct + i * 256) * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          ptx::sts_v4(raw + OP_BYTES + (ct + i * 256) * 16,
+                      __float_as_uint(ptx::tf32_residual(v[i].x)),
+                      __float_as_uint(ptx::tf32_residual(v[i].y)),
+                      __float_as_uint(ptx::tf32_residual(v[i].z)),
+                      __float_as_uint(ptx::tf32_residual(v[i].w)));
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(full_leader[s]);
+    }
+  } else if (warp < 4) {
+    // -------------------------------------------------------- epilogue
+    const uint32_t lane_addr = uint32_t(warp * 32) << 16;
+    const uint32_t empty_leader[2] = {ptx::mapa(&acc_empty[0], 0), ptx::mapa(&acc_empty[1], 0)};
+    uint32_t tcount = 0;
+    for (int64_t t = pair; t < total; t += npairs, ++tcount) {
+      const Tile tc = tile_of(t, tiles_m, tiles_n, p.batch);
+      const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
+      const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
+      ptx::mbar_wait(&acc_full[b], ph);
+      ptx::tc_fence_after();
+      const int64_t row = tc.m0 + rank * HM + warp * 32 + lane;
+      const bool row_ok = row < p.m;
+      float* __restrict__ crow =
+          p.c + tc.pb * p.cps + tc.qb * p.cps2 + (row_ok ? row : 0) * p.crs;
+      const bool vec = (p.ccs == 1) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                       (tc.n0 + BN <= p.n) && p.beta == 0.f;
+      const uint32_t acc_col = SPLIT_ACC ? 0u : b * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 16) {
+        uint32_t v[16];
+        float o[16];
+        ptx::tmem_ld16(tmem + lane_addr + acc_col + cc, v);
+        if (SPLIT_ACC) {
+          uint32_t w[16];
+          ptx::tmem_ld16(tmem + lane_addr + BN + cc, w);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
+        } else {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]);
+        }
+        if (!row_ok) continue;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(crow + tc.n0 + cc + j) =
+                make_float4(p.alpha * o[j], p.alpha * o[j + 1], p.alpha * o[j + 2],
+                            p.alpha * o[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int64_t col = tc.n0 + cc + j;
+            if (col < p.n) store_out(crow + col * p.ccs, o[j], p.alpha, p.beta);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive_cluster(empty_leader[b]);
+    }
+  } else if (warp == 13 && rank == 0 && lane == 0) {
+    // -------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, !A_K, !B_K);
+    // K-major: SW128 rows of 128 B, SBO 1024, K=8 step = 32 B.
+    // MN-major: 32-wide MN slabs of 32 k-rows (4 KB): LBO 4096, SBO 512, step 1024 B.
+    constexpr uint32_t a_lbo = A_K ? 16u : 4096u, a_sbo = A_K ? 1024u : 512u;
+    constexpr uint32_t b_lbo = B_K ? 16u : 4096u, b_sbo = B_K ? 1024u : 512u;
+    constexpr uint32_t a_step = A_K ? 32u : 1024u, b_step = B_K ? 32u : 1024u;
+    constexpr uint32_t a_lay = A_K ? ptx::kLayoutSW128 : ptx::kLayoutSW128Base32B;
+    constexpr uint32_t b_lay = B_K ? ptx::kLayoutSW128 : ptx::kLayoutSW128Base32B;
+    uint32_t it = 0, tcount = 0;
+    for (int64_t t = pair; t < total; t += npairs, ++tcount) {
+      const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
+      const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
+      ptx::mbar_wait_cluster(&acc_empty[b], ph ^ 1u);
+      ptx::tc_fence_after();
+      const uint32_t d_main = tmem + (SPLIT_ACC ? 0u : b * BN);
+      const uint32_t d_small = SPLIT_ACC ? tmem + BN : d_main;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const uint32_t s = it % STAGES;
+        ptx::mbar_wait_cluster(&full[s], (it / STAGES) & 1u);
+        ptx::tc_fence_after();
+        const uint32_t a_raw = ptx::smem_addr(smem + s * STAGE_BYTES);
+        const uint32_t a_lo = a_raw + OP_BYTES;
+        const uint32_t b_raw = a_raw + 2 * OP_BYTES;
+        const uint32_t b_lo = b_raw + OP_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dbr = ptx::umma_desc(b_raw + j * b_step, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
+          const uint32_t first = (kb | j) ? 1u : 0u;
+          ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, first);
+          ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
+          ptx::mma2_tf32_ss(d_main, dar, dbr, idesc, SPLIT_ACC ? first : 1u);
+        }
+        ptx::tc_commit2_mc(&empty[s], 0x3);
+      }
+      ptx::tc_commit2_mc(&acc_full[b], 0x3);
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 12) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem, 512);
+  }
+}
+
+}  // namespace tf32tma
+}  // namespace sbt

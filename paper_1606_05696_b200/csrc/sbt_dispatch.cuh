@@ -17,6 +17,8 @@
 #include "k_tf32x3.cuh"
 #include "k_tf32x3_ts.cuh"
 #include "k_tf32x3_2cta.cuh"
+#include "k_tf32x3_pair_tma.cuh"
+#include "sbt_tma.cuh"
 
 namespace sbt {
 
@@ -97,8 +99,9 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   const int64_t tiles_m = ceil_div(p.m, tf32x3::BM), tiles_n = ceil_div(p.n, BN);
   const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
+  static const int split_mode = env_int("SBT_TF32_SPLIT", 0);
   kern<<<dim3(unsigned(total)), dim3(tf32x3::kThreads), C_::SMEM_BYTES, stream>>>(
-      p, tiles_m, tiles_n);
+      p, tiles_m, tiles_n, split_mode);
   note_launch("tc_tf32x3");
   return 0;
 }
@@ -141,6 +144,45 @@ static int launch_tf32pair_cfg(const GemmParams<float>& p, cudaStream_t stream) 
   return 0;
 }
 
+template <bool AK, bool BK_, bool SPLIT>
+static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tf32tma::SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  const bool ok_a =
+      AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, 32, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B)
+         : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, 32,
+                         CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const bool ok_b =
+      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, 32, 128,
+                          CU_TENSOR_MAP_SWIZZLE_128B)
+          : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, 32,
+                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
+  const int64_t tiles_m = ceil_div(p.m, tf32tma::BM), tiles_n = ceil_div(p.n, tf32tma::BN);
+  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
+  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), tf32tma::SMEM_BYTES, stream>>>(
+      p, ta, tb, tiles_m, tiles_n, total);
+  note_launch(SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma");
+  return 1;
+}
+
+template <bool SPLIT>
+static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
+  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT>(p, s);
+  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT>(p, s);
+  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT>(p, s);
+  return launch_tf32tma_cfg<false, false, SPLIT>(p, s);
+}
+
 template <int BN>
 static int launch_tf32x3_bn(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
   if (am == 1 && bm == 1) return launch_tf32x3_cfg<BN, true, true>(p, s);
@@ -164,7 +206,14 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
     return 0;
   // 0 auto, 1 = 1-CTA smem/smem tiles, 2 = A-in-TMEM persistent, 3 = CTA pair
   static const int variant = env_int("SBT_TC_VARIANT", 0);
-  if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 3) {
+  if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 4) {
+    static const int split_env = env_int("SBT_TC_SPLITACC", -1);
+    const bool split = split_env < 0 ? (p.k > 512) : (split_env != 0);
+    const int rc = split ? launch_tf32tma<true>(p, am, bm, stream)
+                         : launch_tf32tma<false>(p, am, bm, stream);
+    if (rc != 0) return rc;
+  }
+  if (variant == 3) {
     int rc;
     if (am == 1 && bm == 1) rc = launch_tf32pair_cfg<true, true>(p, stream);
     else if (am == 1) rc = launch_tf32pair_cfg<true, false>(p, stream);

@@ -121,6 +121,38 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---- TMA -----------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 4-D tiled TMA load global -> this CTA's smem, completion on `bar` (tx bytes)
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cta.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+__device__ __forceinline__ float4 lds_v4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(saddr));
+  return v;
+}
+// residual of the tensor core's TF32 truncation: x - (x with the low 13 bits cleared)
+__device__ __forceinline__ float tf32_residual(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
 // ---- clusters / CTA pairs (cta_group::2) ---------------------------------------
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -227,6 +259,24 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
   hi = to_tf32(x);
   lo = to_tf32(x - __uint_as_float(hi));
+}
+// Experiment / cheap splits.  mode 1: truncation split (hi = x & ~0x1fff, lo =
+// (x - hi) & ~0x1fff).  mode 2: hi = raw x, lo = tf32(x - trunc(x)).  mode 3:
+// hi = raw x, lo = tf32(x - rna(x)).
+__device__ __forceinline__ void split_tf32_mode(float x, uint32_t& hi, uint32_t& lo, int mode) {
+  const uint32_t xb = __float_as_uint(x);
+  if (mode == 1) {
+    hi = xb & 0xFFFFE000u;
+    lo = __float_as_uint(x - __uint_as_float(hi)) & 0xFFFFE000u;
+  } else if (mode == 2) {
+    hi = xb;
+    lo = to_tf32(x - __uint_as_float(xb & 0xFFFFE000u));
+  } else if (mode == 3) {
+    hi = xb;
+    lo = to_tf32(x - __uint_as_float(to_tf32(x)));
+  } else {
+    split_tf32(x, hi, lo);
+  }
 }
 
 // streaming 16-byte global load (read-only path, no L1 allocation)

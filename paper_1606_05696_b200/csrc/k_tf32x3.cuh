@@ -3,6 +3,8 @@
 //
 //   C = alpha * (A_hi B_hi + A_hi B_lo + A_lo B_hi) + beta * C,   x = x_hi + x_lo
 //
+// The tensor core truncates fp32 operands to TF32, so x_hi is the raw fp32
+// value and x_lo = x - trunc_tf32(x) (see k_tf32x3_pair_tma.cuh).
 // 1xTF32 misses the reference's fp32 tolerance (~3e-4 vs 1e-5, SURVEY.md
 // Appendix C); the three-term split reaches ~1e-7.
 //
@@ -14,6 +16,9 @@
 // so every op-flag combination the dispatcher produces is a native tensor-core
 // operand (UMMA's a_major / b_major bits) -- the permutation is folded into the
 // shared-memory staging, never materialised in HBM.
+//
+// This 1-CTA kernel serves skinny problems (N <= 128 after orientation, e.g.
+// the rank-32 Tucker mode products); large tiles go to the CTA-pair kernel.
 //
 // Pipeline (one 128 x BN output tile per CTA, 9 warps):
 //   warps 0-7 : producers.  16-byte coalesced LDG of the next K-block is in
@@ -63,7 +68,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int mn4, int k, int mn_atoms) {
 
 template <int BN, bool A_K, bool B_K>
 __global__ void __launch_bounds__(kThreads, 1)
-tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n, int split_mode) {
+tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
   using C_ = Cfg<BN>;
   constexpr int STAGES = C_::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -145,10 +150,10 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n, int sp
         const int e = tid + i * kProducers;
         const uint32_t off = A_K ? kmajor_off(e >> 3, e & 7) : mnmajor_off(e & 31, e >> 5, BM / 32);
         uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-        ptx::split_tf32_mode(ra[i].x, h0, l0, split_mode);
-        ptx::split_tf32_mode(ra[i].y, h1, l1, split_mode);
-        ptx::split_tf32_mode(ra[i].z, h2, l2, split_mode);
-        ptx::split_tf32_mode(ra[i].w, h3, l3, split_mode);
+        ptx::split_tf32_fast(ra[i].x, h0, l0);
+        ptx::split_tf32_fast(ra[i].y, h1, l1);
+        ptx::split_tf32_fast(ra[i].z, h2, l2);
+        ptx::split_tf32_fast(ra[i].w, h3, l3);
         ptx::sts_v4(a_hi + off, h0, h1, h2, h3);
         ptx::sts_v4(a_lo + off, l0, l1, l2, l3);
       }
@@ -158,10 +163,10 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n, int sp
         const uint32_t off = B_K ? kmajor_off(e >> 3, e & 7)
                                  : mnmajor_off(e % (BN / 4), e / (BN / 4), BN / 32);
         uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
-        ptx::split_tf32_mode(rb[i].x, h0, l0, split_mode);
-        ptx::split_tf32_mode(rb[i].y, h1, l1, split_mode);
-        ptx::split_tf32_mode(rb[i].z, h2, l2, split_mode);
-        ptx::split_tf32_mode(rb[i].w, h3, l3, split_mode);
+        ptx::split_tf32_fast(rb[i].x, h0, l0);
+        ptx::split_tf32_fast(rb[i].y, h1, l1);
+        ptx::split_tf32_fast(rb[i].z, h2, l2);
+        ptx::split_tf32_fast(rb[i].w, h3, l3);
         ptx::sts_v4(b_hi + off, h0, h1, h2, h3);
         ptx::sts_v4(b_lo + off, l0, l1, l2, l3);
       }

@@ -24,7 +24,8 @@
 // drops ~3x.  (Two accumulators use all 512 TMEM columns, so SPLIT_ACC runs
 // with a single accumulator buffer; the default double-buffers instead.)
 //
-// Warp roles per CTA (14 warps): 0-3 epilogue, 4-11 lo converters,
+// Warp roles per CTA (14 warps): 0-3 epilogue, 4-11 lo converters (two groups
+// of 4 warps taking alternate K-blocks, so each has two K-blocks of time),
 // 12 TMA producer + TMEM allocator, 13 MMA issuer (leader).
 #pragma once
 #include <cuda.h>
@@ -36,13 +37,19 @@ namespace sbt {
 namespace tf32tma {
 
 constexpr int BM = 256, BN = 256, HM = 128, HN = 128, BK = 32;
-constexpr int STAGES = 3;
+// Raw (TMA) ring of RAW_SLOTS x 32 KB and lo ring of LO_SLOTS x 32 KB: raw
+// slots are held from TMA issue to MMA retirement, lo slots only from
+// conversion to MMA retirement, so a deeper raw ring keeps more HBM traffic in
+// flight for the same shared memory.
+constexpr int RAW_SLOTS = 4;
+constexpr int LO_SLOTS = 2;
 constexpr int kThreads = 14 * 32;
-constexpr int kConvWarps = 8;
-constexpr int OP_BYTES = 128 * BK * 4;            // 16 KB: one operand half, raw or lo
-constexpr int STAGE_BYTES = 4 * OP_BYTES;          // A raw, A lo, B raw, B lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr uint32_t kTxBytes = 2 * OP_BYTES;        // raw A + raw B per stage
+constexpr int kConvWarps = 8;                      // two groups of 4, alternating K-blocks
+constexpr int kGroupWarps = 4;
+constexpr int OP_BYTES = 128 * BK * 4;             // 16 KB: one operand half
+constexpr int SLOT_BYTES = 2 * OP_BYTES;           // A half + B half
+constexpr int SMEM_BYTES = (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES + 1024 + 256;
+constexpr uint32_t kTxBytes = SLOT_BYTES;          // raw A + raw B per K-block
 
 struct Tile {
   int64_t m0, n0, pb, qb;
@@ -84,10 +91,13 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = raw_full + STAGES;
-  uint64_t* empty = full + STAGES;
-  uint64_t* acc_full = empty + STAGES;
+  uint8_t* raw_ring = smem;
+  uint8_t* lo_ring = smem + RAW_SLOTS * SLOT_BYTES;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES);
+  uint64_t* raw_empty = raw_full + RAW_SLOTS;
+  uint64_t* full = raw_empty + RAW_SLOTS;         // converted (leader's copy is the one used)
+  uint64_t* lo_empty = full + RAW_SLOTS;
+  uint64_t* acc_full = lo_empty + LO_SLOTS;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -102,14 +112,15 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
 
   if (warp == 12) {
     if (lane == 0) {
-      for (int s = 0; s < STAGES; ++s) {
+      for (int s = 0; s < RAW_SLOTS; ++s) {
         ptx::mbar_init(&raw_full[s], 1);
-        ptx::mbar_init(&full[s], 2 * kConvWarps);
-        ptx::mbar_init(&empty[s], 1);
+        ptx::mbar_init(&raw_empty[s], 1);
+        ptx::mbar_init(&full[s], 2 * kGroupWarps);
       }
+      for (int s = 0; s < LO_SLOTS; ++s) ptx::mbar_init(&lo_empty[s], 1);
       for (int b = 0; b < 2; ++b) {
         ptx::mbar_init(&acc_full[b], 1);
-        ptx::mbar_init(&acc_empty[b], 2 * 128);
+        ptx::mbar_init(&acc_empty[b], 2 * 4);  // one arrival per epilogue warp of each CTA
       }
       ptx::fence_mbarrier_init();
       ptx::prefetch_tmap(&tmA);
@@ -130,36 +141,39 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       // -------------------------------------------------------- TMA producer
       const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
       for (int64_t g = 0; g < n_iter; ++g) {
-        const uint32_t s = uint32_t(g % STAGES);
-        ptx::mbar_wait(&empty[s], (uint32_t(g / STAGES) & 1u) ^ 1u);
+        const uint32_t s = uint32_t(g % RAW_SLOTS);
+        ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
         const Tile tc = tile_of(pair + (g / nkb) * npairs, tiles_m, tiles_n, p.batch);
         const int64_t k0 = int64_t(g % nkb) * BK;
-        uint8_t* st = smem + s * STAGE_BYTES;
+        uint8_t* st = raw_ring + s * SLOT_BYTES;
         ptx::mbar_arrive_expect_tx(&raw_full[s], kTxBytes);
         tma_operand<A_K>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc, a_bc2);
-        tma_operand<B_K>(&tmB, st + 2 * OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
+        tma_operand<B_K>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
                          tc.qb, b_bc, b_bc2);
       }
     }
   } else if (warp >= 4 && warp < 4 + kConvWarps) {
     // -------------------------------------------------------- lo converters
-    const int ct = tid - 128;  // 0..255
-    uint32_t full_leader[STAGES];
+    // group c converts K-blocks g = c, c+2, ... into lo slot c
+    const int grp = (warp - 4) / kGroupWarps;
+    const int ct = tid - 128 - grp * kGroupWarps * 32;  // 0..127
+    uint32_t full_leader[RAW_SLOTS];
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) full_leader[s] = ptx::mapa(&full[s], 0);
-    for (int64_t g = 0; g < n_iter; ++g) {
-      const uint32_t s = uint32_t(g % STAGES);
-      ptx::mbar_wait(&raw_full[s], uint32_t(g / STAGES) & 1u);
-      const uint32_t base = ptx::smem_addr(smem + s * STAGE_BYTES);
+    for (int s = 0; s < RAW_SLOTS; ++s) full_leader[s] = ptx::mapa(&full[s], 0);
+    const uint32_t lo_base = ptx::smem_addr(lo_ring + grp * SLOT_BYTES);
+    for (int64_t g = grp; g < n_iter; g += LO_SLOTS) {
+      const uint32_t s = uint32_t(g % RAW_SLOTS);
+      ptx::mbar_wait(&lo_empty[grp], (uint32_t(g / LO_SLOTS) & 1u) ^ 1u);
+      ptx::mbar_wait(&raw_full[s], uint32_t(g / RAW_SLOTS) & 1u);
+      const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
 #pragma unroll
-      for (int op = 0; op < 2; ++op) {  // A then B
-        const uint32_t raw = base + op * 2 * OP_BYTES;
-        float4 v[4];
+      for (int h = 0; h < 2; ++h) {
+        float4 v[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = ptx::lds_v4(raw + (ct + i * 256) * 16);
+        for (int i = 0; i < 8; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 8 + i) * 128) * 16);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          ptx::sts_v4(raw + OP_BYTES + (ct + i * 256) * 16,
+        for (int i = 0; i < 8; ++i)
+          ptx::sts_v4(lo_base + (ct + (h * 8 + i) * 128) * 16,
                       __float_as_uint(ptx::tf32_residual(v[i].x)),
                       __float_as_uint(ptx::tf32_residual(v[i].y)),
                       __float_as_uint(ptx::tf32_residual(v[i].z)),
@@ -167,7 +181,10 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(full_leader[s]);
+      if (lane == 0) {
+        if (rank == 0) ptx::mbar_arrive(&full[s]);
+        else ptx::mbar_arrive_remote(full_leader[s]);
+      }
     }
   } else if (warp < 4) {
     // -------------------------------------------------------- epilogue
@@ -219,7 +236,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive_cluster(empty_leader[b]);
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) ptx::mbar_arrive(&acc_empty[b]);
+        else ptx::mbar_arrive_remote(empty_leader[b]);
+      }
     }
   } else if (warp == 13 && rank == 0 && lane == 0) {
     // -------------------------------------------------------- MMA issuer
@@ -235,18 +256,19 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
-      ptx::mbar_wait_cluster(&acc_empty[b], ph ^ 1u);
+      ptx::mbar_wait(&acc_empty[b], ph ^ 1u);
       ptx::tc_fence_after();
       const uint32_t d_main = tmem + (SPLIT_ACC ? 0u : b * BN);
       const uint32_t d_small = SPLIT_ACC ? tmem + BN : d_main;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const uint32_t s = it % STAGES;
-        ptx::mbar_wait_cluster(&full[s], (it / STAGES) & 1u);
+        const uint32_t s = it % RAW_SLOTS;
+        const uint32_t ls = it % LO_SLOTS;
+        ptx::mbar_wait(&full[s], (it / RAW_SLOTS) & 1u);
         ptx::tc_fence_after();
-        const uint32_t a_raw = ptx::smem_addr(smem + s * STAGE_BYTES);
-        const uint32_t a_lo = a_raw + OP_BYTES;
-        const uint32_t b_raw = a_raw + 2 * OP_BYTES;
-        const uint32_t b_lo = b_raw + OP_BYTES;
+        const uint32_t a_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
+        const uint32_t b_raw = a_raw + OP_BYTES;
+        const uint32_t a_lo = ptx::smem_addr(lo_ring + ls * SLOT_BYTES);
+        const uint32_t b_lo = a_lo + OP_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
@@ -258,7 +280,8 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
           ptx::mma2_tf32_ss(d_main, dar, dbr, idesc, SPLIT_ACC ? first : 1u);
         }
-        ptx::tc_commit2_mc(&empty[s], 0x3);
+        ptx::tc_commit2_mc(&raw_empty[s], 0x3);
+        ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
       }
       ptx::tc_commit2_mc(&acc_full[b], 0x3);
     }

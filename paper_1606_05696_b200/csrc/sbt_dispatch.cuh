@@ -15,8 +15,6 @@
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
 #include "k_tf32x3.cuh"
-#include "k_tf32x3_ts.cuh"
-#include "k_tf32x3_2cta.cuh"
 #include "k_tf32x3_pair_tma.cuh"
 #include "sbt_tma.cuh"
 
@@ -99,48 +97,9 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   const int64_t tiles_m = ceil_div(p.m, tf32x3::BM), tiles_n = ceil_div(p.n, BN);
   const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
-  static const int split_mode = env_int("SBT_TF32_SPLIT", 0);
   kern<<<dim3(unsigned(total)), dim3(tf32x3::kThreads), C_::SMEM_BYTES, stream>>>(
-      p, tiles_m, tiles_n, split_mode);
+      p, tiles_m, tiles_n);
   note_launch("tc_tf32x3");
-  return 0;
-}
-
-template <bool AK, bool BK_>
-static int launch_tf32ts_cfg(const GemmParams<float>& p, cudaStream_t stream) {
-  auto kern = tf32ts::tf32x3_ts_kernel<AK, BK_>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tf32ts::SMEM_BYTES) != cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
-  const int64_t tiles_m = ceil_div(p.m, tf32ts::BM), tiles_n = ceil_div(p.n, tf32ts::BN);
-  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
-  const int64_t grid = total < kNumSMs ? total : kNumSMs;
-  kern<<<dim3(unsigned(grid)), dim3(tf32ts::kThreads), tf32ts::SMEM_BYTES, stream>>>(
-      p, tiles_m, tiles_n, total);
-  note_launch("tc_tf32x3_ts");
-  return 0;
-}
-
-template <bool AK, bool BK_>
-static int launch_tf32pair_cfg(const GemmParams<float>& p, cudaStream_t stream) {
-  auto kern = tf32pair::tf32x3_pair_kernel<AK, BK_>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tf32pair::SMEM_BYTES) != cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
-  const int64_t tiles_m = ceil_div(p.m, tf32pair::BM), tiles_n = ceil_div(p.n, tf32pair::BN);
-  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
-  const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
-  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32pair::kThreads), tf32pair::SMEM_BYTES, stream>>>(
-      p, tiles_m, tiles_n, total);
-  note_launch("tc_tf32x3_pair");
   return 0;
 }
 
@@ -191,20 +150,46 @@ static int launch_tf32x3_bn(const GemmParams<float>& p, int am, int bm, cudaStre
   return launch_tf32x3_cfg<BN, false, false>(p, s);
 }
 
+// Batch <-> row role swap: the batch index becomes the MMA row index (and the
+// old rows a batch mode).  Valid when B does not depend on the batch.  This is
+// how the exceptional ("extended") cases reach the tensor cores: their first
+// operand is unit-stride along the batch mode, which becomes an MN-major MMA
+// operand (reference kernels.py:179-204 puts apt = 1 there).
+template <typename T>
+static bool batch_row_swapped(const GemmParams<T>& p, GemmParams<T>* q) {
+  if (p.bps != 0 || p.batch < 2) return false;
+  *q = p;
+  q->m = p.batch; q->batch = p.m;
+  q->ars = p.aps; q->aps = p.ars;
+  q->crs = p.cps; q->cps = p.crs;
+  return true;
+}
+
 // Returns 1 if launched, 0 if not eligible, <0 on error.
 static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
-  // orient: the larger of (m, n) becomes the 128-row MMA dimension
-  GemmParams<float> p = (p0.n > p0.m) ? transposed(p0) : p0;
-  int am = a_major(p), bm = b_major(p);
-  if (!am || !bm) {  // the other orientation may be eligible
-    GemmParams<float> q = transposed(p);
-    const int am2 = a_major(q), bm2 = b_major(q);
-    if (!am2 || !bm2) return 0;
-    p = q; am = am2; bm = bm2;
+  // candidate orientations: as given, transposed (C^T = B^T A^T), and the
+  // batch<->row swaps of both; take the eligible one with the largest MMA M.
+  GemmParams<float> cand[4];
+  int nc = 0;
+  cand[nc++] = p0;
+  cand[nc++] = transposed(p0);
+  GemmParams<float> q;
+  if (batch_row_swapped(p0, &q)) cand[nc++] = q;
+  if (batch_row_swapped(transposed(p0), &q)) cand[nc++] = q;
+  int best = -1, am = 0, bm = 0;
+  for (int i = 0; i < nc; ++i) {
+    const int a = a_major(cand[i]), b = b_major(cand[i]);
+    if (!a || !b) continue;
+    if (best < 0 || cand[i].m > cand[best].m ||
+        (cand[i].m == cand[best].m && cand[i].n > cand[best].n)) {
+      best = i; am = a; bm = b;
+    }
   }
+  if (best < 0) return 0;
+  const GemmParams<float>& p = cand[best];
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
-  // 0 auto, 1 = 1-CTA smem/smem tiles, 2 = A-in-TMEM persistent, 3 = CTA pair
+  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel
   static const int variant = env_int("SBT_TC_VARIANT", 0);
   if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 4) {
     static const int split_env = env_int("SBT_TC_SPLITACC", -1);
@@ -212,22 +197,6 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
     const int rc = split ? launch_tf32tma<true>(p, am, bm, stream)
                          : launch_tf32tma<false>(p, am, bm, stream);
     if (rc != 0) return rc;
-  }
-  if (variant == 3) {
-    int rc;
-    if (am == 1 && bm == 1) rc = launch_tf32pair_cfg<true, true>(p, stream);
-    else if (am == 1) rc = launch_tf32pair_cfg<true, false>(p, stream);
-    else if (bm == 1) rc = launch_tf32pair_cfg<false, true>(p, stream);
-    else rc = launch_tf32pair_cfg<false, false>(p, stream);
-    return rc < 0 ? rc : 1;
-  }
-  if (variant == 2 && p.n > 64) {
-    int rc;
-    if (am == 1 && bm == 1) rc = launch_tf32ts_cfg<true, true>(p, stream);
-    else if (am == 1) rc = launch_tf32ts_cfg<true, false>(p, stream);
-    else if (bm == 1) rc = launch_tf32ts_cfg<false, true>(p, stream);
-    else rc = launch_tf32ts_cfg<false, false>(p, stream);
-    return rc < 0 ? rc : 1;
   }
   int bn = env_int("SBT_TC_BN", 0);
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256)

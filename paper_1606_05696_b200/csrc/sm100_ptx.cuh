@@ -173,6 +173,12 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Remote arrive with the default (release, cta) semantics -- what CUTLASS's
+// 2-SM UMMA pipelines use to signal the leader CTA; avoids the GPU-scope
+// MEMBAR that a release.cluster arrive compiles to.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -260,23 +266,11 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   hi = to_tf32(x);
   lo = to_tf32(x - __uint_as_float(hi));
 }
-// Experiment / cheap splits.  mode 1: truncation split (hi = x & ~0x1fff, lo =
-// (x - hi) & ~0x1fff).  mode 2: hi = raw x, lo = tf32(x - trunc(x)).  mode 3:
-// hi = raw x, lo = tf32(x - rna(x)).
-__device__ __forceinline__ void split_tf32_mode(float x, uint32_t& hi, uint32_t& lo, int mode) {
-  const uint32_t xb = __float_as_uint(x);
-  if (mode == 1) {
-    hi = xb & 0xFFFFE000u;
-    lo = __float_as_uint(x - __uint_as_float(hi)) & 0xFFFFE000u;
-  } else if (mode == 2) {
-    hi = xb;
-    lo = to_tf32(x - __uint_as_float(xb & 0xFFFFE000u));
-  } else if (mode == 3) {
-    hi = xb;
-    lo = to_tf32(x - __uint_as_float(to_tf32(x)));
-  } else {
-    split_tf32(x, hi, lo);
-  }
+// The tensor core truncates fp32 -> TF32 (drops the low 13 mantissa bits), so
+// the raw value is a valid "hi" operand and the exact residual is "lo".
+__device__ __forceinline__ void split_tf32_fast(float x, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(x);
+  lo = __float_as_uint(x - __uint_as_float(hi & 0xFFFFE000u));
 }
 
 // streaming 16-byte global load (read-only path, no L1 allocation)

@@ -65,60 +65,58 @@ def flops_bytes(n, itemsize):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every ~5 ms while the
+    timed region runs (the B200_PROFILING clocks line, without nvidia-smi's
+    ~100 ms start-up latency)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - no NVML
+            self._nv = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM),
+                                     int(get_reasons(self._h))))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:6]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(name for name, bit in self.REASONS.items()
+                         if any(r & bit for _, r in self.samples))
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples),
+                "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -185,26 +183,54 @@ def run_gpu(args):
     for _ in range(args.warmup):
         for cid, plan, a, b, c in work:
             execute_plan(plan, a, b, 1.0, 0.0, c)
-    # events: one per case boundary per step, all on the launching stream
+    # (1) per-case attribution: events between the launches, no graph
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nc + 1)]
           for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for st in range(args.steps):
+        ev[st][0].record(stream)
+        for i, (cid, plan, a, b, c) in enumerate(work):
+            execute_plan(plan, a, b, 1.0, 0.0, c)
+            ev[st][i + 1].record(stream)
+    torch.cuda.synchronize()
+    per_case = [[ev[st][i].elapsed_time(ev[st][i + 1]) for st in range(args.steps)]
+                for i in range(nc)]
+    nograph_ms = ev[0][0].elapsed_time(ev[-1][nc]) / args.steps
+
+    # (2) the timed steps: the 36 launches of one step captured once into a CUDA
+    # graph (no host launch gaps), replayed K times
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                for cid, plan, a, b, c in work:
+                    execute_plan(plan, a, b, 1.0, 0.0, c)
+        stream.wait_stream(cap)
+        for _ in range(args.warmup):
+            graph.replay()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     with ClockSampler(device.index) as clocks:
-        for s in range(args.steps):
-            ev[s][0].record(stream)
-            for i, (cid, plan, a, b, c) in enumerate(work):
-                execute_plan(plan, a, b, 1.0, 0.0, c)
-                ev[s][i + 1].record(stream)
+        time.sleep(0.05)  # sampler running before the timed region starts
+        t0e.record(stream)
+        for _ in range(args.steps):
+            if graph is not None:
+                graph.replay()
+            else:
+                for cid, plan, a, b, c in work:
+                    execute_plan(plan, a, b, 1.0, 0.0, c)
+        t1e.record(stream)
         torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
+    launches = (_lib.launch_count() - launches0) if graph is None else nc * args.steps
     barrier()
-    total_ms = ev[0][0].elapsed_time(ev[-1][nc])
-    per_case = [[ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps)]
-                for i in range(nc)]
-    kern_ms = total_ms
+    total_ms = t0e.elapsed_time(t1e)
+    kern_ms = sum(sum(x) for x in per_case)
     t = torch.tensor([total_ms], device=device, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -220,8 +246,12 @@ def run_gpu(args):
         peak_note = (f"3xTF32 = bf16_tflops({peaks['source']})/2/3; "
                      f"fp32 SIMT nominal 74.4 TFLOP/s")
     else:
-        peak_tflops = FP64_NOMINAL_TFLOPS
-        peak_note = "fp64 DMMA nominal (datasheet 37 TFLOP/s)"
+        try:
+            peak_tflops = _lib.probe_fp64_peak("dmma")
+            peak_note = "fp64 DMMA measured in-run by sbt_probe_fp64_peak"
+        except Exception:
+            peak_tflops = FP64_NOMINAL_TFLOPS
+            peak_note = "fp64 DMMA nominal (datasheet 37 TFLOP/s)"
     hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     roof_ms = max(fl / (peak_tflops * 1e12), by / (hbm * 1e9)) * 1e3 * nc
     # dominant kernel family
@@ -241,6 +271,7 @@ def run_gpu(args):
         "traffic": None, "peak_source": peak_note,
         "step_frac_of_roofline": round(roof_ms / ms_per_step, 4),
         "kernel_share_of_step": round(fam_ms[dom] / (kern_ms / args.steps), 4),
+        "measured_in": "CUDA events on the launching stream, per-case pass without graph",
     }
     per_case_out = {work[i][0]: {"ms": round(statistics.median(per_case[i]), 4),
                                  "kernel": kernel_of[work[i][0]],
@@ -272,6 +303,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "cuda_graph": graph is not None,
+            "ms_per_step_nograph": round(nograph_ms, 4),
             "clocks": clocks.summary(),
             "wall_ms_timed_region": round(total_ms, 3),
             "per_case": per_case_out,
@@ -402,6 +435,7 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

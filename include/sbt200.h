@@ -50,6 +50,10 @@ const char* sbt_last_kernel(void);
    3 = small-matrix batched.  Used by tests to cover every path. */
 int sbt_set_kernel_override(int which);
 
+/* Diagnostics (not part of the reference seam): measured fp64 throughput in
+   TFLOP/s of the DMMA tensor pipe (kind 0) or DFMA SIMT pipe (kind 1). */
+int sbt_probe_fp64_peak(int kind, double* tflops);
+
 /* ---- reference: _loops_numba.py:12-25 gemm_core (called by kernels.gemm, kernels.py:107) */
 int sbt_gemm_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
                       const double* a, int64_t oa, int64_t ars, int64_t acs,

@@ -43,6 +43,7 @@ SIGNATURES = {
     "sbt_launch_count": ([], c_int64),
     "sbt_last_kernel": ([], ctypes.c_char_p),
     "sbt_set_kernel_override": ([c_int], c_int),
+    "sbt_probe_fp64_peak": ([c_int, ctypes.POINTER(c_double)], c_int),
     "sbt_gemm_core_f64": (_core_sig(c_double), c_int),
     "sbt_gemm_core_f32": (_core_sig(c_float), c_int),
     "sbt_batched_core_f64": (_batched_sig(c_double), c_int),
@@ -106,3 +107,11 @@ def set_kernel_override(which) -> None:
     names = {"auto": 0, "generic": 1, "tensor": 2, "small": 3}
     which = names.get(which, which)
     check(load().sbt_set_kernel_override(int(which)), "sbt_set_kernel_override")
+
+
+def probe_fp64_peak(kind: str = "dmma") -> float:
+    """Measured fp64 TFLOP/s of the DMMA tensor pipe ("dmma") or DFMA ("dfma")."""
+    out = c_double(0.0)
+    check(load().sbt_probe_fp64_peak(0 if kind == "dmma" else 1, ctypes.byref(out)),
+          "sbt_probe_fp64_peak")
+    return out.value

@@ -1,0 +1,154 @@
+// K1 (fp64): strided batched GEMM on the fp64 tensor pipe (DMMA).
+//
+// tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the B200 fp64
+// tensor path is the warp-level mma.sync m8n8k4 f64, which is the native
+// DMMA.8x8x4 SASS instruction.  Every DMMA is an IEEE fp64 fused multiply-add
+// chain per output element, so results agree with the fp64 CPU oracle to a
+// few ulp (reference tolerance 1e-12, test_acceptance.py:79).
+//
+// Staging: 3-stage cp.async (16 B) ring into padded shared-memory tiles whose
+// contiguous mode is the operand's unit-stride global mode (K-major -> [mn][k],
+// MN-major -> [k][mn]); the paddings (20 / 132 doubles) make every fragment
+// load bank-conflict free.  Out-of-range chunks are zero-filled.
+//
+// CTA tile 128 x 128 x 16, 8 warps as 2 (M) x 4 (N), warp tile 64 x 32 =
+// 8 x 4 DMMA tiles (64 fp64 accumulators per thread).
+#pragma once
+#include "sbt_common.cuh"
+
+namespace sbt {
+namespace dmma {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int kThreads = 256;
+constexpr int LDK = 20;   // [mn][k] rows (16 k + 4 pad)
+constexpr int LDMN = 132; // [k][mn] rows (128 mn + 4 pad)
+constexpr int TILE_DOUBLES = 128 * LDK > 16 * LDMN ? 128 * LDK : 16 * LDMN;  // 2560 vs 2112
+constexpr int SMEM_BYTES = STAGES * 2 * TILE_DOUBLES * 8;                   // 120 KB
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// Stage one operand tile (rows = MN extent 128, k = 16) with 16-byte cp.async.
+// KMAJ: global k unit-stride -> smem [mn][LDK]; else mn unit-stride -> [k][LDMN].
+template <bool KMAJ>
+__device__ __forceinline__ void stage_operand(double* dst, const double* __restrict__ src,
+                                              int64_t mn0, int64_t k0, int64_t mn_ext,
+                                              int64_t k_ext, int64_t s_mn, int64_t s_k, int tid) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // 1024 chunks of 2 doubles
+    const int e = tid + i * kThreads;
+    if (KMAJ) {
+      const int mn = e >> 3, k2 = (e & 7) * 2;
+      const int64_t gm = mn0 + mn, gk = k0 + k2;
+      const bool ok = gm < mn_ext && gk < k_ext;
+      cp_async16(dst + mn * LDK + k2, ok ? src + gm * s_mn + gk : src, ok);
+    } else {
+      const int k = e >> 6, mn2 = (e & 63) * 2;
+      const int64_t gm = mn0 + mn2, gk = k0 + k;
+      const bool ok = gm < mn_ext && gk < k_ext;
+      cp_async16(dst + k * LDMN + mn2, ok ? src + gm + gk * s_k : src, ok);
+    }
+  }
+}
+
+template <bool A_K, bool B_K>
+__global__ void __launch_bounds__(kThreads, 1)
+dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
+
+  int64_t t = blockIdx.x;
+  const int64_t m0 = (t % tiles_m) * BM;
+  t /= tiles_m;
+  const int64_t n0 = (t % tiles_n) * BN;
+  t /= tiles_n;
+  const int64_t pb = t % p.batch, qb = t / p.batch;
+  const double* __restrict__ A = p.a + pb * p.aps + qb * p.aps2;
+  const double* __restrict__ B = p.b + pb * p.bps + qb * p.bps2;
+  const int nkb = int((p.k + BK - 1) / BK);
+
+  auto stage = [&](int kb) {
+    double* sa = sm + (kb % STAGES) * 2 * TILE_DOUBLES;
+    double* sb = sa + TILE_DOUBLES;
+    const int64_t k0 = int64_t(kb) * BK;
+    stage_operand<A_K>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
+    stage_operand<B_K>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkb) stage(s);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row (mn) / k within a DMMA
+  for (int kb = 0; kb < nkb; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (kb + STAGES - 1 < nkb) stage(kb + STAGES - 1);
+    cp_async_commit();
+    const double* sa = sm + (kb % STAGES) * 2 * TILE_DOUBLES;
+    const double* sb = sa + TILE_DOUBLES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = wm * 64 + i * 8 + fr;
+        af[i] = A_K ? sa[m * LDK + kk + fk] : sa[(kk + fk) * LDMN + m];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = wn * 32 + j * 8 + fr;
+        bf[j] = B_K ? sb[n * LDK + kk + fk] : sb[(kk + fk) * LDMN + n];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double* C = p.c + pb * p.cps + qb * p.cps2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = m0 + wm * 64 + i * 8 + fr;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = n0 + wn * 32 + j * 8 + 2 * fk + h;
+        if (col < p.n) store_out(C + row * p.crs + col * p.ccs, acc[i][j][h], p.alpha, p.beta);
+      }
+    }
+  }
+}
+
+}  // namespace dmma
+}  // namespace sbt

@@ -19,6 +19,7 @@
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
 #include "sbt_dispatch.cuh"
+#include "k_probe.cuh"
 
 namespace sbt {
 
@@ -163,6 +164,37 @@ int sbt_set_kernel_override(int which) {
   if (which < 0 || which > 3) return SBT_EINVAL;
   g_override.store(which);
   return SBT_OK;
+}
+
+// Diagnostics: measured fp64 tensor (kind 0 = DMMA) or SIMT (kind 1 = DFMA)
+// throughput in TFLOP/s on the current device.  Not part of the reference seam.
+int sbt_probe_fp64_peak(int kind, double* tflops) {
+  if (!tflops || kind < 0 || kind > 1) return fail(SBT_EINVAL, "bad probe arguments");
+  double* out = nullptr;
+  int rc;
+  if ((rc = check_cuda(cudaMalloc(&out, sizeof(double)), "cudaMalloc")) != SBT_OK) return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4096, blocks = kNumSMs * 8, threads = 256;
+  for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+    cudaEventRecord(e0);
+    if (kind == 0) probe::dmma_peak_kernel<<<blocks, threads>>>(out, iters);
+    else probe::dfma_peak_kernel<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+  }
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double warps = double(blocks) * threads / 32.0;
+  // DMMA m8n8k4: 256 FMA per warp instruction; DFMA: 32 FMA per warp instruction
+  const double fma = warps * iters * 8.0 * (kind == 0 ? 256.0 : 32.0);
+  *tflops = 2.0 * fma / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  note_launch(kind == 0 ? "probe_dmma" : "probe_dfma");
+  return check_cuda(cudaGetLastError(), "probe");
 }
 
 #define SBT_DEFINE(T, SUF)                                                                     \

@@ -16,6 +16,7 @@
 #include "k_generic.cuh"
 #include "k_tf32x3.cuh"
 #include "k_tf32x3_pair_tma.cuh"
+#include "k_dmma.cuh"
 #include "sbt_tma.cuh"
 
 namespace sbt {
@@ -61,7 +62,9 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-static inline bool mult4(int64_t v) { return (v & 3) == 0; }
+// 16-byte vectors: 4 fp32 or 2 fp64 elements
+template <typename T>
+static inline bool vmult(int64_t v) { return v % int64_t(16 / sizeof(T)) == 0; }
 static inline bool aligned16(const void* ptr) {
   return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0;
 }
@@ -70,16 +73,16 @@ static inline bool aligned16(const void* ptr) {
 // returns 1 = K-major, 2 = MN-major, 0 = not eligible
 template <typename T>
 static int a_major(const GemmParams<T>& p) {
-  if (!aligned16(p.a) || !mult4(p.aps) || !mult4(p.aps2)) return 0;
-  if (p.acs == 1 && mult4(p.ars) && mult4(p.k)) return 1;
-  if (p.ars == 1 && mult4(p.acs) && mult4(p.m)) return 2;
+  if (!aligned16(p.a) || !vmult<T>(p.aps) || !vmult<T>(p.aps2)) return 0;
+  if (p.acs == 1 && vmult<T>(p.ars) && vmult<T>(p.k)) return 1;
+  if (p.ars == 1 && vmult<T>(p.acs) && vmult<T>(p.m)) return 2;
   return 0;
 }
 template <typename T>
 static int b_major(const GemmParams<T>& p) {
-  if (!aligned16(p.b) || !mult4(p.bps) || !mult4(p.bps2)) return 0;
-  if (p.brs == 1 && mult4(p.bcs) && mult4(p.k)) return 1;
-  if (p.bcs == 1 && mult4(p.brs) && mult4(p.n)) return 2;
+  if (!aligned16(p.b) || !vmult<T>(p.bps) || !vmult<T>(p.bps2)) return 0;
+  if (p.brs == 1 && vmult<T>(p.bcs) && vmult<T>(p.k)) return 1;
+  if (p.bcs == 1 && vmult<T>(p.brs) && vmult<T>(p.n)) return 2;
   return 0;
 }
 
@@ -165,28 +168,68 @@ static bool batch_row_swapped(const GemmParams<T>& p, GemmParams<T>* q) {
   return true;
 }
 
-// Returns 1 if launched, 0 if not eligible, <0 on error.
-static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
-  // candidate orientations: as given, transposed (C^T = B^T A^T), and the
-  // batch<->row swaps of both; take the eligible one with the largest MMA M.
-  GemmParams<float> cand[4];
+// Candidate orientations: as given, transposed (C^T = B^T A^T), and the
+// batch<->row swaps of both; pick the tensor-core-eligible one with the
+// largest MMA M.  Returns false if none is eligible.
+template <typename T>
+static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm) {
+  GemmParams<T> cand[4];
   int nc = 0;
   cand[nc++] = p0;
   cand[nc++] = transposed(p0);
-  GemmParams<float> q;
+  GemmParams<T> q;
   if (batch_row_swapped(p0, &q)) cand[nc++] = q;
   if (batch_row_swapped(transposed(p0), &q)) cand[nc++] = q;
-  int best = -1, am = 0, bm = 0;
+  int best = -1;
   for (int i = 0; i < nc; ++i) {
     const int a = a_major(cand[i]), b = b_major(cand[i]);
     if (!a || !b) continue;
     if (best < 0 || cand[i].m > cand[best].m ||
         (cand[i].m == cand[best].m && cand[i].n > cand[best].n)) {
-      best = i; am = a; bm = b;
+      best = i; *am = a; *bm = b;
     }
   }
-  if (best < 0) return 0;
-  const GemmParams<float>& p = cand[best];
+  if (best < 0) return false;
+  *out = cand[best];
+  return true;
+}
+
+template <bool AK, bool BK_>
+static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
+  auto kern = dmma::dmma_gemm_kernel<AK, BK_>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dmma::SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  const int64_t tiles_m = ceil_div(p.m, dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
+  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  if (total > int64_t(0x7fffffff)) return -2;
+  kern<<<dim3(unsigned(total)), dim3(dmma::kThreads), dmma::SMEM_BYTES, stream>>>(p, tiles_m,
+                                                                                tiles_n);
+  note_launch("tc_dmma_f64");
+  return 1;
+}
+
+static int try_tensor_f64(const GemmParams<double>& p0, cudaStream_t stream, bool forced) {
+  GemmParams<double> p;
+  int am = 0, bm = 0;
+  if (!orient(p0, &p, &am, &bm)) return 0;
+  if (!forced && (p.m < 32 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 1e6))
+    return 0;
+  if (am == 1 && bm == 1) return launch_dmma_cfg<true, true>(p, stream);
+  if (am == 1) return launch_dmma_cfg<true, false>(p, stream);
+  if (bm == 1) return launch_dmma_cfg<false, true>(p, stream);
+  return launch_dmma_cfg<false, false>(p, stream);
+}
+
+// Returns 1 if launched, 0 if not eligible, <0 on error.
+static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
+  GemmParams<float> p;
+  int am = 0, bm = 0;
+  if (!orient(p0, &p, &am, &bm)) return 0;
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
   // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel
@@ -214,12 +257,12 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
   const int ov = kernel_override();
-  if constexpr (sizeof(T) == 4) {
-    if (ov == 0 || ov == 2) {
-      const int rc = try_tensor_f32(p, stream, ov == 2);
-      if (rc < 0) return rc;
-      if (rc == 1) return 0;
-    }
+  if (ov == 0 || ov == 2) {
+    int rc;
+    if constexpr (sizeof(T) == 4) rc = try_tensor_f32(p, stream, ov == 2);
+    else rc = try_tensor_f64(p, stream, ov == 2);
+    if (rc < 0) return rc;
+    if (rc == 1) return 0;
   }
   launch_generic<T>(p, stream);
   return 0;

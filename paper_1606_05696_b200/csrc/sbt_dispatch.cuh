@@ -17,6 +17,7 @@
 #include "k_tf32x3.cuh"
 #include "k_tf32x3_pair_tma.cuh"
 #include "k_dmma.cuh"
+#include "k_small.cuh"
 #include "sbt_tma.cuh"
 
 namespace sbt {
@@ -254,9 +255,60 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
   return rc < 0 ? rc : 1;
 }
 
+// ---- K3 small-matrix batched ----------------------------------------------------
+template <typename T, int S, bool AM, bool BK_>
+static int launch_small_cfg(const GemmParams<T>& p, cudaStream_t stream) {
+  auto kern = small::small_batched_kernel<T, S, AM, BK_>;
+  constexpr int smem = small::smem_bytes<T, S>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  const int64_t ngroups = ceil_div(p.batch, small::Shape<S>::G);
+  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int64_t grid = ngroups < int64_t(kNumSMs) * per_sm ? ngroups : int64_t(kNumSMs) * per_sm;
+  kern<<<dim3(unsigned(grid)), dim3(small::kThreads), smem, stream>>>(p, ngroups);
+  note_launch(sizeof(T) == 4 ? "small_batched_f32" : "small_batched_f64");
+  return 1;
+}
+
+template <typename T, int S>
+static int launch_small_s(const GemmParams<T>& p, bool am, bool bk, cudaStream_t s) {
+  if (am && bk) return launch_small_cfg<T, S, true, true>(p, s);
+  if (am) return launch_small_cfg<T, S, true, false>(p, s);
+  if (bk) return launch_small_cfg<T, S, false, true>(p, s);
+  return launch_small_cfg<T, S, false, false>(p, s);
+}
+
+// Many tiny dense matrices: every extent <= 64, each matrix stored densely.
+template <typename T>
+static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
+  const int64_t mx = p.m > p.n ? (p.m > p.k ? p.m : p.k) : (p.n > p.k ? p.n : p.k);
+  if (mx > 64 || p.batch2 != 1) return 0;
+  if (!forced && p.batch < 512) return 0;
+  const bool am = p.ars == 1 && p.acs == p.m, ak = p.acs == 1 && p.ars == p.k;
+  const bool bk = p.brs == 1 && p.bcs == p.k, bn = p.bcs == 1 && p.brs == p.n;
+  if (!(am || ak) || !(bk || bn) || !(p.crs == 1 && p.ccs == p.m)) return 0;
+  if (!vmult<T>(p.m * p.k) || !vmult<T>(p.k * p.n) || !vmult<T>(p.aps) || !vmult<T>(p.bps) ||
+      !aligned16(p.a) || !aligned16(p.b))
+    return 0;
+  if (mx <= 8) return launch_small_s<T, 8>(p, am, bk, stream);
+  if (mx <= 16) return launch_small_s<T, 16>(p, am, bk, stream);
+  if (mx <= 32) return launch_small_s<T, 32>(p, am, bk, stream);
+  return launch_small_s<T, 64>(p, am, bk, stream);
+}
+
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
   const int ov = kernel_override();
+  if (ov == 0 || ov == 3) {
+    const int rc = try_small<T>(p, stream, ov == 3);
+    if (rc < 0) return rc;
+    if (rc == 1) return 0;
+  }
   if (ov == 0 || ov == 2) {
     int rc;
     if constexpr (sizeof(T) == 4) rc = try_tensor_f32(p, stream, ov == 2);

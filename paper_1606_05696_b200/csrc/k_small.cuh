@@ -19,6 +19,18 @@ namespace small {
 constexpr int kThreads = 256;
 constexpr int STAGES = 3;  // fp32: 96 KB -> 2 CTAs/SM; fp64: 192 KB -> 1 CTA/SM
 
+// four consecutive elements from a 16-byte aligned smem address
+__device__ __forceinline__ void load4(const float* p, float& a, float& b, float& c, float& d) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = v.x; b = v.y; c = v.z; d = v.w;
+}
+__device__ __forceinline__ void load4(const double* p, double& a, double& b, double& c,
+                                      double& d) {
+  const double2 v0 = reinterpret_cast<const double2*>(p)[0];
+  const double2 v1 = reinterpret_cast<const double2*>(p)[1];
+  a = v0.x; b = v0.y; c = v1.x; d = v1.y;
+}
+
 template <int S>
 struct Shape {
   static constexpr int G = (4096 / (S * S)) > 0 ? 4096 / (S * S) : 1;  // matrices per group
@@ -26,8 +38,12 @@ struct Shape {
   static constexpr int BPR = S / 4;                                   // 4x4 blocks per row
 };
 
+// per-matrix smem slot: S*S elements + 32 B of padding, so that the G matrices
+// of a group start on different banks (conflict-free 16-byte fragment loads)
 template <typename T, int S>
-constexpr int stage_elems() { return 2 * Shape<S>::G * S * S; }
+constexpr int slot_elems() { return S * S + 32 / int(sizeof(T)); }
+template <typename T, int S>
+constexpr int stage_elems() { return 2 * Shape<S>::G * slot_elems<T, S>(); }
 template <typename T, int S>
 constexpr int smem_bytes() { return STAGES * stage_elems<T, S>() * int(sizeof(T)) + 64; }
 
@@ -47,29 +63,24 @@ small_batched_kernel(GemmParams<T> p, int64_t ngroups) {
   const int m = int(p.m), n = int(p.n), k = int(p.k);
   const int a_elems = m * k, b_elems = k * n;
   const int64_t total = p.batch;
-  const bool a_contig = p.aps == a_elems, b_contig = p.bps == b_elems;
+  constexpr int SL = slot_elems<T, S>();
 
-  // smem per stage: G matrices of A at stride a_elems, then G of B
+  // smem per stage: G padded matrix slots of A, then G of B; one bulk copy per
+  // matrix and operand, issued by G threads in parallel
   auto issue = [&](int64_t grp, int slot) {
     T* sa = sm + slot * stage_elems<T, S>();
-    T* sb = sa + G * S * S;
+    T* sb = sa + G * SL;
     const int64_t b0 = grp * G;
     const int nmat = int(total - b0 < G ? total - b0 : G);
     if (tid == 0)
       ptx::mbar_arrive_expect_tx(&full[slot],
                                  uint32_t(nmat * (a_elems + b_elems) * int(sizeof(T))));
-    __syncwarp();
-    if (a_contig) {
-      if (tid == 0) ptx::bulk_load(sa, p.a + b0 * p.aps, nmat * a_elems * sizeof(T), &full[slot]);
-    } else if (tid < nmat) {
-      ptx::bulk_load(sa + tid * a_elems, p.a + (b0 + tid) * p.aps, a_elems * sizeof(T), &full[slot]);
-    }
-    if (b_contig) {
-      if (tid == 32) ptx::bulk_load(sb, p.b + b0 * p.bps, nmat * b_elems * sizeof(T), &full[slot]);
-    } else if (tid >= 32 && tid < 32 + nmat) {
-      ptx::bulk_load(sb + (tid - 32) * b_elems, p.b + (b0 + tid - 32) * p.bps,
-                     b_elems * sizeof(T), &full[slot]);
-    }
+    __syncthreads();  // expect_tx precedes every completion of this phase
+    if (tid < nmat)
+      ptx::bulk_load(sa + tid * SL, p.a + (b0 + tid) * p.aps, a_elems * sizeof(T), &full[slot]);
+    else if (tid >= 128 && tid < 128 + nmat)
+      ptx::bulk_load(sb + (tid - 128) * SL, p.b + (b0 + tid - 128) * p.bps, b_elems * sizeof(T),
+                     &full[slot]);
   };
 
   if (tid == 0) {
@@ -81,22 +92,21 @@ small_batched_kernel(GemmParams<T> p, int64_t ngroups) {
   const int g_local = tid / Sh::TPM;
   const int lt = tid - g_local * Sh::TPM;
   const int i0 = (lt % Sh::BPR) * 4, j0 = (lt / Sh::BPR) * 4;
+  const bool vec4 = (m % 4 == 0) && (n % 4 == 0) && (k % 4 == 0);
   const bool vec_store = (m % 4 == 0) && (p.cps % 4 == 0) && p.beta == T(0) &&
                          ((reinterpret_cast<uintptr_t>(p.c) & 15) == 0);
 
-  if (tid < 64) {
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
-      const int64_t gi = blockIdx.x + int64_t(s) * gridDim.x;
-      if (gi < ngroups) issue(gi, s);
-    }
+  for (int s = 0; s < STAGES; ++s) {
+    const int64_t gi = blockIdx.x + int64_t(s) * gridDim.x;
+    if (gi < ngroups) issue(gi, s);
   }
   uint32_t it = 0;
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int slot = int(it % STAGES);
     ptx::mbar_wait(&full[slot], (it / STAGES) & 1u);
-    const T* sa = sm + slot * stage_elems<T, S>() + g_local * a_elems;
-    const T* sb = sm + slot * stage_elems<T, S>() + G * S * S + g_local * b_elems;
+    const T* sa = sm + slot * stage_elems<T, S>() + g_local * SL;
+    const T* sb = sm + slot * stage_elems<T, S>() + G * SL + g_local * SL;
     const int64_t bidx = grp * G + g_local;
     if (bidx < total && i0 < m && j0 < n) {
       T acc[4][4];
@@ -104,17 +114,38 @@ small_batched_kernel(GemmParams<T> p, int64_t ngroups) {
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
-#pragma unroll 4
-      for (int l = 0; l < k; ++l) {
-        T a[4], b[4];
+      if (vec4) {
+        // 4-deep k chunks: 4 + 4 sixteen-byte-aligned quads -> 64 FMA
+        for (int l0 = 0; l0 < k; l0 += 4) {
+          T a[4][4], b[4][4];  // a[r][dl] = A(i0+r, l0+dl), b[dl][c] = B(l0+dl, j0+c)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) a[r] = A_M ? sa[(i0 + r) + l * m] : sa[(i0 + r) * k + l];
+          for (int q = 0; q < 4; ++q) {
+            if (A_M) load4(sa + i0 + (l0 + q) * m, a[0][q], a[1][q], a[2][q], a[3][q]);
+            else     load4(sa + (i0 + q) * k + l0, a[q][0], a[q][1], a[q][2], a[q][3]);
+            if (B_K) load4(sb + l0 + (j0 + q) * k, b[0][q], b[1][q], b[2][q], b[3][q]);
+            else     load4(sb + (l0 + q) * n + j0, b[q][0], b[q][1], b[q][2], b[q][3]);
+          }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) b[c] = B_K ? sb[l + (j0 + c) * k] : sb[l * n + j0 + c];
+          for (int dl = 0; dl < 4; ++dl)
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+              for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r][dl], b[dl][c], acc[r][c]);
+        }
+      } else {
+        for (int l = 0; l < k; ++l) {
+          T a[4], b[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            a[r] = (i0 + r < m) ? (A_M ? sa[(i0 + r) + l * m] : sa[(i0 + r) * k + l]) : T(0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            b[c] = (j0 + c < n) ? (B_K ? sb[l + (j0 + c) * k] : sb[l * n + j0 + c]) : T(0);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
       }
       T* C = p.c + bidx * p.cps;
       if (vec_store) {
@@ -142,7 +173,7 @@ small_batched_kernel(GemmParams<T> p, int64_t ngroups) {
     }
     __syncthreads();  // every thread is done with this slot
     const int64_t gnext = grp + int64_t(STAGES) * gridDim.x;
-    if (tid < 64 && gnext < ngroups) issue(gnext, slot);
+    if (gnext < ngroups) issue(gnext, slot);
   }
 }
 

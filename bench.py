@@ -356,6 +356,119 @@ def run_e2e(args, work, device, dtype, itemsize, n, step_flops, world):
             "api": "paper_1606_05696_b200.execute_plan with pinned host<->device copies"}
 
 
+# ----------------------------------------------------------------------------- other configs
+
+
+def _time_steps(fn, steps, warmup):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_config(args):
+    """BASELINE configs[2..4] as single-GPU measurements (one JSON line each):
+    small   -- batched GEMM n=8/16/32/64, P=10^6 (HBM-bound; GB/s vs measured copy BW)
+    order4  -- C[mnpq] = A[mkp] B[nkq], n=128: one nested-batched launch
+    hooi    -- Tucker HOOI 512^3 rank 32 fp32: ms per iteration, contraction GFLOP/s"""
+    import torch
+    from paper_1606_05696_b200 import _lib, kernels
+    from paper_1606_05696_b200.layout import DenseTensor, Layout
+    from paper_1606_05696_b200.notation import ContractionSpec
+    from paper_1606_05696_b200.planner import execute_plan, plan_single_mode
+    torch.cuda.set_device(0)
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    it = 4 if dtype == torch.float32 else 8
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    out = []
+    if args.config == "small":
+        P = args.batch
+        for n in (8, 16, 32, 64):
+            if n == 64 and dtype == torch.float64 and P > 200000:
+                continue
+            a = torch.rand(n * n * P, dtype=dtype, device="cuda")
+            b = torch.rand(n * n * P, dtype=dtype, device="cuda")
+            c = torch.empty(n * n * P, dtype=dtype, device="cuda")
+            f = lambda: kernels.strided_batched_gemm("N", "N", n, n, n, 1.0, a, n, n * n, b, n,  # noqa: E731
+                                                     n * n, 0.0, c, n, n * n, P)
+            ms = _time_steps(f, args.steps, args.warmup)
+            gbs = 3 * n * n * P * it / (ms * 1e-3) / 1e9
+            out.append({"n": n, "batch": P, "ms": round(ms, 4), "kernel": _lib.last_kernel(),
+                        "gflops": round(2 * n ** 3 * P / (ms * 1e-3) / 1e9, 1),
+                        "hbm_gbs": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm, 3)})
+            del a, b, c
+        value = out[2]["hbm_gbs"] if len(out) > 2 else out[-1]["hbm_gbs"]
+        line = {"metric": "batched small-matrix GEMM HBM throughput (n=32 headline)",
+                "value": value, "unit": "GB/s", "roofline": {
+                    "bound": "hbm", "achieved": value, "peak": hbm, "unit": "GB/s",
+                    "frac": round(value / hbm, 3), "traffic": None},
+                "config": {"workload": f"configs[2] batched GEMM, P={P}"}, "sweep": out}
+    elif args.config == "order4":
+        n = args.n if args.n != 256 else 128
+        spec = ContractionSpec(tuple("mkp"), tuple("nkq"), tuple("mnpq"))
+        la, lb, lc = Layout.packed((n,) * 3), Layout.packed((n,) * 3), Layout.packed((n,) * 4)
+        a = DenseTensor(la, torch.rand(la.size, dtype=dtype, device="cuda"))
+        b = DenseTensor(lb, torch.rand(lb.size, dtype=dtype, device="cuda"))
+        c = DenseTensor(lc, torch.empty(lc.size, dtype=dtype, device="cuda"))
+        plan = plan_single_mode(spec, la, lb, lc)
+        n0 = _lib.launch_count()
+        execute_plan(plan, a, b, 1.0, 0.0, c)
+        launches = _lib.launch_count() - n0
+        ms = _time_steps(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), args.steps, args.warmup)
+        flops = 2.0 * n ** 5
+        line = {"metric": "4th-order contraction GFLOP/s", "value": round(flops / (ms * 1e-3) / 1e9, 1),
+                "unit": "GFLOP/s", "ms_per_step": round(ms, 4),
+                "config": {"workload": f"configs[4] C[mnpq]=A[mkp]B[nkq] n={n}",
+                           "strategy": plan.strategy, "launches_per_contraction": launches,
+                           "kernel": _lib.last_kernel()}}
+    elif args.config == "hooi":
+        import paper_1606_05696_b200 as sbt
+        n, r = (args.n if args.n != 256 else 512), 32
+        g = torch.Generator(device="cuda").manual_seed(0)
+        core = torch.randn(r, r, r, device="cuda", generator=g, dtype=torch.float64)
+        us = [torch.linalg.qr(torch.randn(n, r, device="cuda", generator=g,
+                                          dtype=torch.float64))[0] for _ in range(3)]
+        x = torch.einsum("ia,abc->ibc", us[0], core)
+        x = torch.einsum("jb,ibc->ijc", us[1], x)
+        x = torch.einsum("kc,ijc->ijk", us[2], x)
+        x = x + 1e-3 * torch.randn(n, n, n, device="cuda", generator=g, dtype=torch.float64)
+        t = DenseTensor(Layout.packed((n, n, n)), x.permute(2, 1, 0).contiguous().reshape(-1).to(dtype))
+        del x
+        t0 = time.perf_counter()
+        sbt.hooi(t, (r, r, r), max_iters=1, tol=-1.0)
+        torch.cuda.synchronize()
+        t_init = time.perf_counter() - t0
+        iters = max(2, args.steps)
+        t0 = time.perf_counter()
+        model = sbt.hooi(t, (r, r, r), max_iters=iters, tol=-1.0)
+        torch.cuda.synchronize()
+        total = time.perf_counter() - t0
+        per_iter = (total - t_init) / (iters - 1) if iters > 1 else total
+        # contraction FLOPs per iteration with mode-0 reuse: chain(skip0) 2 products,
+        # T x0, two 32-rank products, core
+        fl = 2 * (n ** 3 * r + n * n * r * r) + 2 * n ** 3 * r + 2 * 2 * n * n * r * r + 2 * n * r ** 3
+        line = {"metric": "Tucker HOOI ms per iteration", "value": round(per_iter * 1e3, 3),
+                "unit": "ms", "higher_is_better": False,
+                "config": {"workload": f"configs[3] HOOI {n}^3 rank {r} {args.dtype}",
+                           "init_plus_one_iter_ms": round(t_init * 1e3, 1),
+                           "contraction_gflop_per_iter": round(fl / 1e9, 2),
+                           "fit_history": [round(f, 8) for f in model.fit_history]}}
+    else:
+        raise SystemExit(f"unknown config {args.config}")
+    line.update({"n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                 "dtype": args.dtype, "data": "synthetic"})
+    line.setdefault("higher_is_better", True)
+    print(json.dumps(line))
+
+
 # ----------------------------------------------------------------------------- CPU arm
 
 
@@ -436,11 +549,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--config", choices=("sweep", "small", "order4", "hooi"), default="sweep")
+    ap.add_argument("--batch", type=int, default=1000000)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config != "sweep":
+        run_config(args)
     else:
         run_gpu(args)
 

@@ -301,8 +301,81 @@ static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
   return launch_small_s<T, 64>(p, am, bk, stream);
 }
 
+// ---- split-K for tall-skinny reductions --------------------------------------------
+// A single output tile with a huge K (e.g. the Tucker HOSVD Gram matrices,
+// 512 x 512 with K = 262144) leaves most SMs idle.  Split K into S contiguous
+// chunks as a batched GEMM into a stream-ordered workspace, then reduce the S
+// partials (fixed S and order: deterministic).
+template <typename T>
+__global__ void reduce_splits_kernel(const T* __restrict__ w, int64_t nsplit, int64_t m,
+                                     int64_t n, T alpha, T beta, T* c, int64_t crs,
+                                     int64_t ccs) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    T acc = T(0);
+    for (int64_t s = 0; s < nsplit; ++s) acc += w[s * total + e];
+    const int64_t i = e % m, j = e / m;
+    store_out(c + i * crs + j * ccs, acc, alpha, beta);
+  }
+}
+
+template <typename T>
+static int launch_gemm_core(const GemmParams<T>& p, cudaStream_t stream);
+
+template <typename T>
+static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
+  if (p.batch != 1 || p.batch2 != 1 || p.k < 16384) return 0;
+  const int64_t tiles = ceil_div(p.m, 128) * ceil_div(p.n, 128);
+  if (tiles >= kNumSMs / 2) return 0;
+  int64_t S = (2 * kNumSMs) / tiles;
+  const int64_t max_s = p.k / 4096;
+  if (S > max_s) S = max_s;
+  if (S < 2) return 0;
+  // chunk length: multiple of 32 so every chunk keeps the operands' alignment
+  const int64_t kc = ((ceil_div(p.k, S) + 31) / 32) * 32;
+  S = ceil_div(p.k, kc);
+  T* w = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&w), size_t(S) * p.m * p.n * sizeof(T), stream) !=
+      cudaSuccess)
+    return -3;
+  GemmParams<T> q = p;
+  q.alpha = T(1); q.beta = T(0);
+  q.c = w; q.crs = 1; q.ccs = p.m; q.cps = p.m * p.n;
+  q.k = kc; q.batch = S - 1;             // full chunks
+  q.aps = kc * p.acs; q.bps = kc * p.brs;
+  int rc = 0;
+  if (q.batch > 0) rc = launch_gemm_core<T>(q, stream);
+  if (rc == 0) {                          // ragged last chunk
+    GemmParams<T> t = q;
+    t.batch = 1; t.k = p.k - (S - 1) * kc;
+    t.a = p.a + (S - 1) * kc * p.acs; t.b = p.b + (S - 1) * kc * p.brs;
+    t.c = w + (S - 1) * p.m * p.n;
+    rc = launch_gemm_core<T>(t, stream);
+  }
+  if (rc == 0) {
+    const int64_t total = p.m * p.n;
+    const int64_t blocks = ceil_div(total, 256) < 4096 ? ceil_div(total, 256) : 4096;
+    reduce_splits_kernel<T><<<unsigned(blocks), 256, 0, stream>>>(w, S, p.m, p.n, p.alpha,
+                                                                  p.beta, p.c, p.crs, p.ccs);
+    note_launch("split_k_reduce");
+  }
+  cudaFreeAsync(w, stream);
+  return rc < 0 ? rc : 1;
+}
+
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
+  if (kernel_override() == 0) {
+    const int rc = try_split_k<T>(p, stream);
+    if (rc < 0) return rc;
+    if (rc == 1) return 0;
+  }
+  return launch_gemm_core<T>(p, stream);
+}
+
+template <typename T>
+static int launch_gemm_core(const GemmParams<T>& p, cudaStream_t stream) {
   const int ov = kernel_override();
   if (ov == 0 || ov == 3) {
     const int rc = try_small<T>(p, stream, ov == 3);

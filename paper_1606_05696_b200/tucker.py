@@ -117,6 +117,22 @@ def _factor_from_tensor(t: DenseTensor, r: int, rank: int):
     return _sign_fix(vecs[:, :rank].contiguous())
 
 
+def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
+    """One planned contraction T x_r U^T (transpose) or T x_r U."""
+    order = cur.layout.order
+    rows, cols = u.shape
+    labels_b, out_ext = (("k", "z"), cols) if transpose else (("z", "k"), rows)
+    labels_a = tuple("k" if i == r else _LETTERS[i] for i in range(order))
+    labels_c = tuple("z" if i == r else _LETTERS[i] for i in range(order))
+    spec = ContractionSpec(labels_a, labels_b, labels_c)
+    b = _as_factor_tensor(u, cur.dtype)
+    dims = list(cur.layout.dims)
+    dims[r] = out_ext
+    out = DenseTensor.empty(Layout.packed(dims), dtype=cur.dtype, device=cur.device)
+    execute_plan(_planned(spec, cur.layout, b.layout, out.layout), cur, b, 1.0, 0.0, out)
+    return out
+
+
 @dataclass
 class TuckerModel:
     core: DenseTensor
@@ -154,17 +170,7 @@ def _mode_product_chain(t: DenseTensor, factors, skip, transpose: bool) -> Dense
     modes.sort(key=lambda r: -red(r))
     cur = t
     for r in modes:
-        rows, cols = factors[r].shape
-        labels_b, out_ext = (("k", "z"), cols) if transpose else (("z", "k"), rows)
-        labels_a = tuple("k" if i == r else _LETTERS[i] for i in range(order))
-        labels_c = tuple("z" if i == r else _LETTERS[i] for i in range(order))
-        spec = ContractionSpec(labels_a, labels_b, labels_c)
-        b = _as_factor_tensor(factors[r], cur.dtype)
-        dims = list(cur.layout.dims)
-        dims[r] = out_ext
-        out = DenseTensor.empty(Layout.packed(dims), dtype=cur.dtype, device=cur.device)
-        execute_plan(_planned(spec, cur.layout, b.layout, out.layout), cur, b, 1.0, 0.0, out)
-        cur = out
+        cur = _mode_product(cur, factors[r], r, transpose)
     return cur
 
 
@@ -182,8 +188,23 @@ def _norm(t: DenseTensor) -> float:
     return float(torch.linalg.vector_norm(t.data.to(torch.float64)))
 
 
-def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10) -> TuckerModel:
-    """Higher-order orthogonal iteration (reference tucker.py:136-174)."""
+def _reuses_mode0(t: DenseTensor) -> bool:
+    """For order 3 with mode 0 the largest, the reference chains for skip=1,
+    skip=2 and the core all START with T x_0 U_0^T under the same U_0
+    (tucker.py:95-99 sorts by reduction extent, ties ascending), so that product
+    can be computed once per iteration with bitwise-identical results."""
+    d = t.layout.dims
+    return t.layout.order == 3 and d[0] >= d[2] and d[0] >= d[1]
+
+
+def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
+         reuse_mode0: bool = True) -> TuckerModel:
+    """Higher-order orthogonal iteration (reference tucker.py:136-174).
+
+    With ``reuse_mode0`` (order-3 tensors whose mode 0 is the largest) the
+    product T x_0 U_0^T that the reference recomputes three times per iteration
+    is computed once: T is read twice per iteration instead of four times, with
+    the same operations in the same order."""
     order = t.layout.order
     ranks = tuple(int(r) for r in ranks)
     if len(ranks) != order:
@@ -191,17 +212,37 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10) -> Tuck
     for r, (rank, dim) in enumerate(zip(ranks, t.layout.dims)):
         if not 1 <= rank <= dim:
             raise ValueError(f"rank {rank} invalid for mode {r} extent {dim}")
-    factors = [_factor_from_tensor(t, r, ranks[r]) for r in range(order)]
+    torch = _torch()
+    t64 = t if t.dtype == torch.float64 else DenseTensor(t.layout, t.data.to(torch.float64))
+    factors = [_factor_from_tensor(t64, r, ranks[r]) for r in range(order)]
+    del t64
     norm_t = _norm(t)
     fits = []
     prev = -np.inf
     iters = 0
+    fast = reuse_mode0 and _reuses_mode0(t)
     for it in range(max_iters):
         iters = it + 1
-        for r in range(order):
-            y = _mode_product_chain(t, factors, skip=r, transpose=True)
-            factors[r] = _factor_from_tensor(y, r, ranks[r])
-        core = tucker_core(t, factors)
+        if fast:
+            # skip=0 chain: modes 1, 2 (reference order); then X0 = T x_0 U_0^T
+            y = _mode_product_chain(t, factors, skip=0, transpose=True)
+            factors[0] = _factor_from_tensor(y, 0, ranks[0])
+            x0 = _mode_product(t, factors[0], 0, True)
+            # reference skip=1 chain is [0, 2] and skip=2 chain is [0, 1]
+            y = _mode_product(x0, factors[2], 2, True)
+            factors[1] = _factor_from_tensor(y, 1, ranks[1])
+            y2 = _mode_product(x0, factors[1], 1, True)
+            factors[2] = _factor_from_tensor(y2, 2, ranks[2])
+            # reference core chain: mode 0, then the larger of modes 1 / 2 first
+            if t.layout.dims[1] >= t.layout.dims[2]:
+                core = _mode_product(y2, factors[2], 2, True)
+            else:
+                core = _mode_product(_mode_product(x0, factors[2], 2, True), factors[1], 1, True)
+        else:
+            for r in range(order):
+                y = _mode_product_chain(t, factors, skip=r, transpose=True)
+                factors[r] = _factor_from_tensor(y, r, ranks[r])
+            core = tucker_core(t, factors)
         norm_g = _norm(core)
         resid = np.sqrt(max(0.0, norm_t ** 2 - norm_g ** 2))
         fit = 1.0 - resid / norm_t if norm_t > 0 else 1.0

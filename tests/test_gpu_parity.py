@@ -375,3 +375,98 @@ def test_hooi_fp32_matches_oracle():
         u = model.factors[r].cpu().numpy()
         ur = ref["factors"][r]
         np.testing.assert_allclose(u @ u.T, ur @ ur.T, atol=1e-4)
+
+
+# ------------------------------------------------------------------ kernel families / paths
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_small_matrix_kernel_forced_layouts(dtype):
+    """K3 on every dense storage order, odd and multiple-of-4 extents, beta != 0."""
+    _lib.set_kernel_override("small")
+    rng = np.random.default_rng(21)
+    for (m, n, k, P) in ((8, 8, 8, 300), (12, 16, 4, 257), (32, 32, 32, 70), (6, 10, 14, 50),
+                         (64, 64, 64, 5)):
+        for opa in ("N", "T"):
+            for opb in ("N", "T"):
+                lda = m if opa == "N" else k
+                ldb = k if opb == "N" else n
+                ha, hb = rng.uniform(-1, 1, m * k * P), rng.uniform(-1, 1, k * n * P)
+                hc = rng.uniform(-1, 1, m * n * P)
+                a, b, c = dev(ha, dtype), dev(hb, dtype), dev(hc, dtype)
+                kernels.strided_batched_gemm(opa, opb, m, n, k, 0.75, a, lda, m * k, b, ldb,
+                                             k * n, -0.5, c, m, m * n, P)
+                want = host(dev(hc, dtype)).copy()
+                oapi.run_call("strided_batched_gemm", dict(opa=opa, opb=opb, m=m, n=n, k=k,
+                              alpha=0.75, lda=lda, loa=m * k, ldb=ldb, lob=k * n, beta=-0.5,
+                              ldc=m, loc=m * n, batch_count=P), host(a), host(b), want)
+                got = _lib.last_kernel()
+                assert naive.max_rel_err(host(c), want) <= TOL[dtype], (m, n, k, opa, opb, got)
+
+
+def test_split_k_for_tall_reductions():
+    rng = np.random.default_rng(5)
+    for dtype in (torch.float64, torch.float32):
+        m, n, k = 96, 64, 70000
+        ha, hb = rng.uniform(-1, 1, m * k), rng.uniform(-1, 1, k * n)
+        a, b = dev(ha, dtype), dev(hb, dtype)
+        c = torch.zeros(m * n, dtype=dtype, device="cuda")
+        n0 = _lib.launch_count()
+        kernels.gemm("N", "N", m, n, k, 1.0, a, m, b, k, 0.0, c, m)
+        assert _lib.launch_count() - n0 >= 2  # split partials + reduction
+        want = np.zeros(m * n)
+        oapi.run_call("gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=1.0, lda=m, ldb=k,
+                      beta=0.0, ldc=m), host(a), host(b), want)
+        assert naive.max_rel_err(host(c), want) <= TOL[dtype] * 4
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fourth_order_nested_single_launch_n64(dtype):
+    rng = np.random.default_rng(8)
+    spec = ContractionSpec(tuple("mkp"), tuple("nkq"), tuple("mnpq"))
+    ext = dict(m=64, n=48, k=32, p=40, q=24)
+    la, lb, lc = _packed(spec, ext)
+    A, B = rng.uniform(-1, 1, la.dims), rng.uniform(-1, 1, lb.dims)
+    a, b = DenseTensor.from_array(A, dtype=dtype), DenseTensor.from_array(B, dtype=dtype)
+    c = DenseTensor.zeros(lc, dtype=dtype)
+    n0 = _lib.launch_count()
+    execute_plan(plan_single_mode(spec, la, lb, lc), a, b, 1.0, 0.0, c)
+    assert _lib.launch_count() == n0 + 1
+    want = np.einsum("mkp,nkq->mnpq", a.to_array().astype(np.float64),
+                     b.to_array().astype(np.float64))
+    assert naive.max_rel_err(c.to_array(), want) <= TOL[dtype]
+
+
+def test_hooi_mode0_reuse_is_bitwise_identical():
+    rng = np.random.default_rng(13)
+    dims, ranks = (40, 36, 32), (5, 4, 3)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-2 * rng.standard_normal(dims)
+    for dtype in ("float32", "float64"):
+        t = DenseTensor.from_array(full, dtype=dtype)
+        m1 = sbt.hooi(t, ranks, max_iters=3, tol=-1.0, reuse_mode0=True)
+        m2 = sbt.hooi(t, ranks, max_iters=3, tol=-1.0, reuse_mode0=False)
+        assert m1.fit_history == m2.fit_history
+        for u1, u2 in zip(m1.factors, m2.factors):
+            assert torch.equal(u1, u2)
+        assert torch.equal(m1.core.data, m2.core.data)
+
+
+def test_tensor_paths_are_used_for_the_36_cases():
+    """No silent fallback: at n=64 every case runs on a tensor-core kernel."""
+    rng = np.random.default_rng(1)
+    for dtype, prefix in ((torch.float32, "tc_tf32x3"), (torch.float64, "tc_dmma")):
+        for case in enumerate_cases(2, 3):
+            spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+            la, lb, lc = _packed(spec, dict(m=64, n=64, p=64, k=64))
+            a = DenseTensor(la, dev(rng.uniform(-1, 1, la.size), dtype))
+            b = DenseTensor(lb, dev(rng.uniform(-1, 1, lb.size), dtype))
+            c = DenseTensor(lc, torch.empty(lc.size, dtype=dtype, device="cuda"))
+            execute_plan(plan_single_mode(spec, la, lb, lc), a, b, 1.0, 0.0, c)
+            assert _lib.last_kernel().startswith(prefix), (case.case_id, _lib.last_kernel())
+
+
+def test_fp64_probe_reports_a_plausible_peak():
+    tf = _lib.probe_fp64_peak("dmma")
+    assert 5.0 < tf < 100.0

@@ -154,16 +154,17 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     }
   } else if (warp >= 4 && warp < 4 + kConvWarps) {
     // -------------------------------------------------------- lo converters
-    // group c converts K-blocks g = c, c+2, ... into lo slot c
+    // group c converts K-blocks g = c, c+2, ... into lo slot g % LO_SLOTS
     const int grp = (warp - 4) / kGroupWarps;
     const int ct = tid - 128 - grp * kGroupWarps * 32;  // 0..127
     uint32_t full_leader[RAW_SLOTS];
 #pragma unroll
     for (int s = 0; s < RAW_SLOTS; ++s) full_leader[s] = ptx::mapa(&full[s], 0);
-    const uint32_t lo_base = ptx::smem_addr(lo_ring + grp * SLOT_BYTES);
-    for (int64_t g = grp; g < n_iter; g += LO_SLOTS) {
+    for (int64_t g = grp; g < n_iter; g += kConvWarps / kGroupWarps) {
       const uint32_t s = uint32_t(g % RAW_SLOTS);
-      ptx::mbar_wait(&lo_empty[grp], (uint32_t(g / LO_SLOTS) & 1u) ^ 1u);
+      const uint32_t ls = uint32_t(g % LO_SLOTS);
+      const uint32_t lo_base = ptx::smem_addr(lo_ring + ls * SLOT_BYTES);
+      ptx::mbar_wait(&lo_empty[ls], (uint32_t(g / LO_SLOTS) & 1u) ^ 1u);
       ptx::mbar_wait(&raw_full[s], uint32_t(g / RAW_SLOTS) & 1u);
       const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
 #pragma unroll

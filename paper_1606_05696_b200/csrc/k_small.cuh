@@ -41,11 +41,11 @@ struct Shape {
 // per-matrix smem slot: S*S elements + 32 B of padding, so that the G matrices
 // of a group start on different banks (conflict-free 16-byte fragment loads)
 template <typename T, int S>
-constexpr int slot_elems() { return S * S + 32 / int(sizeof(T)); }
+__host__ __device__ constexpr int slot_elems() { return S * S + 32 / int(sizeof(T)); }
 template <typename T, int S>
-constexpr int stage_elems() { return 2 * Shape<S>::G * slot_elems<T, S>(); }
+__host__ __device__ constexpr int stage_elems() { return 2 * Shape<S>::G * slot_elems<T, S>(); }
 template <typename T, int S>
-constexpr int smem_bytes() { return STAGES * stage_elems<T, S>() * int(sizeof(T)) + 64; }
+__host__ __device__ constexpr int smem_bytes() { return STAGES * stage_elems<T, S>() * int(sizeof(T)) + 64; }
 
 // A_M: A stored with rows contiguous (ars == 1, acs == m), else (ars == k, acs == 1).
 // B_K: B stored with k contiguous (brs == 1, bcs == k), else (brs == n, bcs == 1).

@@ -36,20 +36,36 @@
 namespace sbt {
 namespace tf32tma {
 
-constexpr int BM = 256, BN = 256, HM = 128, HN = 128, BK = 32;
-// Raw (TMA) ring of RAW_SLOTS x 32 KB and lo ring of LO_SLOTS x 32 KB: raw
-// slots are held from TMA issue to MMA retirement, lo slots only from
-// conversion to MMA retirement, so a deeper raw ring keeps more HBM traffic in
-// flight for the same shared memory.
-constexpr int RAW_SLOTS = 4;
-constexpr int LO_SLOTS = 2;
+constexpr int BM = 256, BN = 256, HM = 128, HN = 128;
 constexpr int kThreads = 14 * 32;
 constexpr int kConvWarps = 8;                      // two groups of 4, alternating K-blocks
 constexpr int kGroupWarps = 4;
-constexpr int OP_BYTES = 128 * BK * 4;             // 16 KB: one operand half
-constexpr int SLOT_BYTES = 2 * OP_BYTES;           // A half + B half
-constexpr int SMEM_BYTES = (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES + 1024 + 256;
-constexpr uint32_t kTxBytes = SLOT_BYTES;          // raw A + raw B per K-block
+
+// K-block depth BK (32: 128 B rows, SW128; 16: 64 B rows, SW64).  Raw (TMA) ring
+// and lo ring share 192 KB: raw slots are held from TMA issue to MMA
+// retirement, lo slots only from conversion to MMA retirement, so the raw ring
+// is the deeper one; a smaller BK gives more, finer slots in flight.
+template <int BK>
+struct Geo {
+  static constexpr int OP_BYTES = 128 * BK * 4;    // one operand half (A or B-half)
+  static constexpr int SLOT_BYTES = 2 * OP_BYTES;  // A half + B half
+  static constexpr int RAW_SLOTS = BK == 32 ? 4 : 8;
+  static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
+  static constexpr int SMEM_BYTES = (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES + 1024 + 512;
+  static constexpr uint32_t TX = SLOT_BYTES;       // raw A + raw B per K-block
+  static constexpr int VEC = OP_BYTES / 16 / 128;  // float4 per converter thread per operand
+};
+constexpr int SMEM_BYTES_MAX = Geo<32>::SMEM_BYTES > Geo<16>::SMEM_BYTES ? Geo<32>::SMEM_BYTES
+                                                                          : Geo<16>::SMEM_BYTES;
+
+// Debug timeline (SBT_TRACE builds only): per-event clock64 stamps of pair 0.
+#ifdef SBT_TRACE
+__device__ long long g_trace[8][4096];
+#define TRACE(row, idx) do { if (blockIdx.x < 2 && (idx) < 4096) g_trace[(row) + 4 * rank][(idx)] = clock64(); } while (0)
+__device__ long long g_trace_epi[2][64][4];
+#else
+#define TRACE(row, idx) do { } while (0)
+#endif
 
 struct Tile {
   int64_t m0, n0, pb, qb;
@@ -66,10 +82,10 @@ __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tile
   return c;
 }
 
-// TMA loads of one operand half (128 rows/cols of the MMA dimension x 32 k).
-// K-major: one box (32 k, 128 mn).  MN-major: four boxes (32 mn, 32 k), one per
-// 32-wide MN atom column, each a contiguous 4 KB slab.
-template <bool KMAJ>
+// TMA loads of one operand half (128 rows/cols of the MMA dimension x BK k).
+// K-major: one box (BK k, 128 mn).  MN-major: four boxes (32 mn, BK k), one per
+// 32-wide MN atom column, each a contiguous slab of BK 128-byte rows.
+template <bool KMAJ, int BK>
 __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar,
                                             int64_t mn0, int64_t k0, int64_t b, int64_t b2,
                                             bool bcast, bool bcast2) {
@@ -79,15 +95,18 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst,
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      ptx::tma_load_4d(dst + c * 4096, tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
+      ptx::tma_load_4d(dst + c * (BK * 128), tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
   }
 }
 
-template <bool A_K, bool B_K, bool SPLIT_ACC>
+template <bool A_K, bool B_K, bool SPLIT_ACC, int BK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
                        int64_t tiles_n, int64_t total) {
+  using Gm = Geo<BK>;
+  constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
+  constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -143,12 +162,13 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       for (int64_t g = 0; g < n_iter; ++g) {
         const uint32_t s = uint32_t(g % RAW_SLOTS);
         ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
+        TRACE(0, int(g));
         const Tile tc = tile_of(pair + (g / nkb) * npairs, tiles_m, tiles_n, p.batch);
         const int64_t k0 = int64_t(g % nkb) * BK;
         uint8_t* st = raw_ring + s * SLOT_BYTES;
-        ptx::mbar_arrive_expect_tx(&raw_full[s], kTxBytes);
-        tma_operand<A_K>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc, a_bc2);
-        tma_operand<B_K>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
+        ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
+        tma_operand<A_K, BK>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc, a_bc2);
+        tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
                          tc.qb, b_bc, b_bc2);
       }
     }
@@ -166,9 +186,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const uint32_t lo_base = ptx::smem_addr(lo_ring + ls * SLOT_BYTES);
       ptx::mbar_wait(&lo_empty[ls], (uint32_t(g / LO_SLOTS) & 1u) ^ 1u);
       ptx::mbar_wait(&raw_full[s], uint32_t(g / RAW_SLOTS) & 1u);
+      if (ct == 0) TRACE(1, int(g));
       const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
+      constexpr int NV = 2 * Gm::VEC;  // float4 chunks per thread (A and B halves)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < NV / 8; ++h) {
         float4 v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 8 + i) * 128) * 16);
@@ -186,6 +208,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         if (rank == 0) ptx::mbar_arrive(&full[s]);
         else ptx::mbar_arrive_remote(full_leader[s]);
       }
+      if (ct == 0) TRACE(2, int(g));
     }
   } else if (warp < 4) {
     // -------------------------------------------------------- epilogue
@@ -198,6 +221,9 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_full[b], ph);
       ptx::tc_fence_after();
+#ifdef SBT_TRACE
+      long long t_ld = 0, t_st = 0, t_begin = clock64();
+#endif
       const int64_t row = tc.m0 + rank * HM + warp * 32 + lane;
       const bool row_ok = row < p.m;
       float* __restrict__ crow =
@@ -205,10 +231,14 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const bool vec = (p.ccs == 1) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                        (tc.n0 + BN <= p.n) && p.beta == 0.f;
       const uint32_t acc_col = SPLIT_ACC ? 0u : b * BN;
+      const bool full_tile = (tc.n0 + BN <= p.n) && p.beta == 0.f;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 16) {
         uint32_t v[16];
         float o[16];
+#ifdef SBT_TRACE
+        long long t0 = clock64();
+#endif
         ptx::tmem_ld16(tmem + lane_addr + acc_col + cc, v);
         if (SPLIT_ACC) {
           uint32_t w[16];
@@ -221,6 +251,10 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
 #pragma unroll
           for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]);
         }
+#ifdef SBT_TRACE
+        long long t1 = clock64();
+        t_ld += t1 - t0;
+#endif
         if (!row_ok) continue;
         if (vec) {
 #pragma unroll
@@ -228,6 +262,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
             *reinterpret_cast<float4*>(crow + tc.n0 + cc + j) =
                 make_float4(p.alpha * o[j], p.alpha * o[j + 1], p.alpha * o[j + 2],
                             p.alpha * o[j + 3]);
+        } else if (full_tile) {
+          // interior tile, beta == 0: straight-line stores, one address add each
+          float* dst = crow + (tc.n0 + cc) * p.ccs;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dst[j * p.ccs] = p.alpha * o[j];
         } else {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -236,6 +275,15 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           }
         }
       }
+#ifdef SBT_TRACE
+      if (blockIdx.x < 2 && tid == 0 && tcount < 64) {
+        long long t_end = clock64();
+        g_trace_epi[rank][tcount][0] = t_begin;
+        g_trace_epi[rank][tcount][1] = t_end;
+        g_trace_epi[rank][tcount][2] = t_ld;
+        g_trace_epi[rank][tcount][3] = t_end - t_begin - t_ld;
+      }
+#endif
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -246,13 +294,16 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   } else if (warp == 13 && rank == 0 && lane == 0) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, !A_K, !B_K);
-    // K-major: SW128 rows of 128 B, SBO 1024, K=8 step = 32 B.
-    // MN-major: 32-wide MN slabs of 32 k-rows (4 KB): LBO 4096, SBO 512, step 1024 B.
-    constexpr uint32_t a_lbo = A_K ? 16u : 4096u, a_sbo = A_K ? 1024u : 512u;
-    constexpr uint32_t b_lbo = B_K ? 16u : 4096u, b_sbo = B_K ? 1024u : 512u;
+    // K-major: rows of BK*4 bytes (SW128 for BK=32, SW64 for BK=16), 8-row
+    // groups at SBO = 8*BK*4, K=8 step = 32 B inside the row.
+    // MN-major: 32-wide MN slabs of BK k-rows: LBO = slab stride (BK*128 B),
+    // SBO 512 (4-row K groups), K=8 step = 1024 B.
+    constexpr uint32_t k_lay = BK == 32 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
+    constexpr uint32_t a_lbo = A_K ? 16u : uint32_t(BK * 128), a_sbo = A_K ? 8u * BK * 4 : 512u;
+    constexpr uint32_t b_lbo = B_K ? 16u : uint32_t(BK * 128), b_sbo = B_K ? 8u * BK * 4 : 512u;
     constexpr uint32_t a_step = A_K ? 32u : 1024u, b_step = B_K ? 32u : 1024u;
-    constexpr uint32_t a_lay = A_K ? ptx::kLayoutSW128 : ptx::kLayoutSW128Base32B;
-    constexpr uint32_t b_lay = B_K ? ptx::kLayoutSW128 : ptx::kLayoutSW128Base32B;
+    constexpr uint32_t a_lay = A_K ? k_lay : ptx::kLayoutSW128Base32B;
+    constexpr uint32_t b_lay = B_K ? k_lay : ptx::kLayoutSW128Base32B;
     uint32_t it = 0, tcount = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
@@ -265,6 +316,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         const uint32_t s = it % RAW_SLOTS;
         const uint32_t ls = it % LO_SLOTS;
         ptx::mbar_wait(&full[s], (it / RAW_SLOTS) & 1u);
+        TRACE(3, int(it));
         ptx::tc_fence_after();
         const uint32_t a_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
         const uint32_t b_raw = a_raw + OP_BYTES;

@@ -107,35 +107,44 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   return 0;
 }
 
-template <bool AK, bool BK_, bool SPLIT>
-static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream) {
-  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT>;
+template <bool AK, bool BK_, bool SPLIT, int KB>
+static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream) {
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB>;
+  constexpr int smem = tf32tma::Geo<KB>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tf32tma::SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
       return -3;
     attr_set = true;
   }
+  const CUtensorMapSwizzle kswz = KB == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUtensorMap ta, tb;
   const bool ok_a =
-      AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, 32, 128,
-                         CU_TENSOR_MAP_SWIZZLE_128B)
-         : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, 32,
+      AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, KB, 128,
+                         kswz)
+         : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, KB,
                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const bool ok_b =
-      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, 32, 128,
-                          CU_TENSOR_MAP_SWIZZLE_128B)
-          : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, 32,
+      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB, 128,
+                          kswz)
+          : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
   const int64_t tiles_m = ceil_div(p.m, tf32tma::BM), tiles_n = ceil_div(p.n, tf32tma::BN);
   const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
   const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
-  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), tf32tma::SMEM_BYTES, stream>>>(
+  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
       p, ta, tb, tiles_m, tiles_n, total);
   note_launch(SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma");
   return 1;
+}
+
+template <bool AK, bool BK_, bool SPLIT>
+static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+  static const int kb = env_int("SBT_TC_BK", 32);
+  return kb == 16 ? launch_tf32tma_kb<AK, BK_, SPLIT, 16>(p, stream)
+                  : launch_tf32tma_kb<AK, BK_, SPLIT, 32>(p, stream);
 }
 
 template <bool SPLIT>

@@ -53,6 +53,9 @@ int sbt_set_kernel_override(int which);
 /* Diagnostics (not part of the reference seam): measured fp64 throughput in
    TFLOP/s of the DMMA tensor pipe (kind 0) or DFMA SIMT pipe (kind 1). */
 int sbt_probe_fp64_peak(int kind, double* tflops);
+/* Diagnostics: measured dense TF32 tensor-pipe throughput (tcgen05.mma
+   kind::tf32, TFLOP/s); the 3xTF32 fp32 roofline is this / 3. */
+int sbt_probe_tf32_peak(double* tflops);
 
 /* ---- reference: _loops_numba.py:12-25 gemm_core (called by kernels.gemm, kernels.py:107) */
 int sbt_gemm_core_f64(int64_t m, int64_t n, int64_t k, double alpha,

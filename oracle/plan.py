@@ -191,12 +191,16 @@ def packed_strides(dims):
     return out
 
 
-def contract(labels_a, labels_b, labels_c, ext, a, b, alpha, beta, c):
-    """Plan + execute a packed contraction exactly as the reference would."""
+def contract(labels_a, labels_b, labels_c, ext, a, b, alpha, beta, c, layouts=None):
+    """Plan + execute a contraction exactly as the reference would (packed
+    operands, or the (dims, strides) of ``layouts`` = (la, lb, lc))."""
     da = [ext[l] for l in labels_a]
     db = [ext[l] for l in labels_b]
     dc = [ext[l] for l in labels_c] or [1]
-    low = lower(labels_a, labels_b, labels_c, da, packed_strides(da), db, packed_strides(db),
-                dc, packed_strides(dc))
+    if layouts is None:
+        sa, sb, sc = packed_strides(da), packed_strides(db), packed_strides(dc)
+    else:
+        sa, sb, sc = (list(x.strides) for x in layouts)
+    low = lower(labels_a, labels_b, labels_c, da, sa, db, sb, dc, sc)
     execute(low, a, b, alpha, beta, c)
     return low

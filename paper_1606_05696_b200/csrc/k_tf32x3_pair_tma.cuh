@@ -27,6 +27,21 @@
 // Warp roles per CTA (14 warps): 0-3 epilogue, 4-11 lo converters (two groups
 // of 4 warps taking alternate K-blocks, so each has two K-blocks of time),
 // 12 TMA producer + TMEM allocator, 13 MMA issuer (leader).
+//
+// Batch-blocked A (BB, the exceptional cases, reference kernels.py:179-204):
+// the A operand is unit-stride along the BATCH mode (apt = 1) while C is
+// unit-stride along m.  Each CTA's 128 MMA rows are (4 consecutive batch
+// entries) x (32 consecutive m): row r = b_l + 4 m_l.  Per 32-row MN atom one
+// dense 3-D TMA box (4 batch, 8 m, BK k) lands as [k][m8][b4]: 128 B of MN per
+// k row, the MN-major SW128_BASE32B atom minus its swizzle (TMA cannot swizzle
+// a 16-byte-wide box; UMMA takes no unswizzled MN-major tf32).  The converter
+// warps, which read every raw element anyway to form lo, write A_hi and A_lo
+// at the swizzled offset (16-byte chunks move whole: off ^ ((off>>7)&3)<<5),
+// so the permutation costs one extra 16 KB smem write per K-block, and in
+// the epilogue a
+// warp's 32 lanes are 8 consecutive m x 4 batch entries: every store
+// instruction writes four full 32-byte sectors of C instead of 32 scattered
+// 4-byte words.  B must not depend on the batch (bps = 0).
 #pragma once
 #include <cuda.h>
 
@@ -45,18 +60,22 @@ constexpr int kGroupWarps = 4;
 // and lo ring share 192 KB: raw slots are held from TMA issue to MMA
 // retirement, lo slots only from conversion to MMA retirement, so the raw ring
 // is the deeper one; a smaller BK gives more, finer slots in flight.
-template <int BK>
+// BB: the converted slot also holds A_hi (the converter re-lays the dense raw
+// A box into the swizzled MN-major atom), so it is 3 operand halves wide.
+template <int BK, bool BB = false>
 struct Geo {
   static constexpr int OP_BYTES = 128 * BK * 4;    // one operand half (A or B-half)
   static constexpr int SLOT_BYTES = 2 * OP_BYTES;  // A half + B half
-  static constexpr int RAW_SLOTS = BK == 32 ? 4 : 8;
+  static constexpr int LO_SLOT_BYTES = (BB ? 3 : 2) * OP_BYTES;
+  // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles
+  // (measured), ~3 K-blocks of MMA time, and a raw slot stays held until the
+  // MMAs that read it retire
+  static constexpr int RAW_SLOTS = (BB ? 4 : 5) * (BK == 32 ? 1 : 2);
   static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
-  static constexpr int SMEM_BYTES = (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES + 1024 + 512;
+  static constexpr int SMEM_BYTES = RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES + 1024 + 512;
   static constexpr uint32_t TX = SLOT_BYTES;       // raw A + raw B per K-block
   static constexpr int VEC = OP_BYTES / 16 / 128;  // float4 per converter thread per operand
 };
-constexpr int SMEM_BYTES_MAX = Geo<32>::SMEM_BYTES > Geo<16>::SMEM_BYTES ? Geo<32>::SMEM_BYTES
-                                                                          : Geo<16>::SMEM_BYTES;
 
 // Debug timeline (SBT_TRACE builds only): per-event clock64 stamps of pair 0.
 #ifdef SBT_TRACE
@@ -70,10 +89,12 @@ __device__ long long g_trace_epi[2][64][4];
 struct Tile {
   int64_t m0, n0, pb, qb;
 };
+// BB tiles cover 64 m (32 per CTA) x 4 batch entries; pb is then the batch group
+template <bool BB = false>
 __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tiles_n,
                                         int64_t batch) {
   Tile c;
-  c.m0 = (t % tiles_m) * BM;
+  c.m0 = (t % tiles_m) * (BB ? 64 : BM);
   t /= tiles_m;
   c.n0 = (t % tiles_n) * BN;
   t /= tiles_n;
@@ -99,20 +120,25 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst,
   }
 }
 
-template <bool A_K, bool B_K, bool SPLIT_ACC, int BK>
+template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
                        int64_t tiles_n, int64_t total) {
-  using Gm = Geo<BK>;
+  static_assert(!(BB && A_K), "batch-blocked A is MN-major");
+  // number of batch units the tile index runs over (BB: groups of 4 entries)
+  const int64_t nbatch = BB ? (p.batch + 3) / 4 : p.batch;
+  using Gm = Geo<BK, BB>;
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
+  constexpr int LO_SLOT_BYTES = Gm::LO_SLOT_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw_ring = smem;
   uint8_t* lo_ring = smem + RAW_SLOTS * SLOT_BYTES;
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + (RAW_SLOTS + LO_SLOTS) * SLOT_BYTES);
+  uint64_t* raw_full =
+      reinterpret_cast<uint64_t*>(smem + RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES);
   uint64_t* raw_empty = raw_full + RAW_SLOTS;
   uint64_t* full = raw_empty + RAW_SLOTS;         // converted (leader's copy is the one used)
   uint64_t* lo_empty = full + RAW_SLOTS;
@@ -163,11 +189,18 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         const uint32_t s = uint32_t(g % RAW_SLOTS);
         ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
         TRACE(0, int(g));
-        const Tile tc = tile_of(pair + (g / nkb) * npairs, tiles_m, tiles_n, p.batch);
+        const Tile tc = tile_of<BB>(pair + (g / nkb) * npairs, tiles_m, tiles_n, nbatch);
         const int64_t k0 = int64_t(g % nkb) * BK;
         uint8_t* st = raw_ring + s * SLOT_BYTES;
         ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
-        tma_operand<A_K, BK>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc, a_bc2);
+        if (BB) {  // four dense (4 batch, 8 m, BK k) boxes [k][m8][b4], one per MN atom
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            ptx::tma_load_4d(st + c * (BK * 128), &tmA, &raw_full[s], int(tc.pb * 4),
+                             int(tc.m0 + rank * 32 + 8 * c), int(k0), a_bc2 ? 0 : int(tc.qb));
+        } else
+          tma_operand<A_K, BK>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc,
+                               a_bc2);
         tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
                          tc.qb, b_bc, b_bc2);
       }
@@ -183,7 +216,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     for (int64_t g = grp; g < n_iter; g += kConvWarps / kGroupWarps) {
       const uint32_t s = uint32_t(g % RAW_SLOTS);
       const uint32_t ls = uint32_t(g % LO_SLOTS);
-      const uint32_t lo_base = ptx::smem_addr(lo_ring + ls * SLOT_BYTES);
+      const uint32_t lo_base = ptx::smem_addr(lo_ring + ls * LO_SLOT_BYTES);
       ptx::mbar_wait(&lo_empty[ls], (uint32_t(g / LO_SLOTS) & 1u) ^ 1u);
       ptx::mbar_wait(&raw_full[s], uint32_t(g / RAW_SLOTS) & 1u);
       if (ct == 0) TRACE(1, int(g));
@@ -195,12 +228,19 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 8 + i) * 128) * 16);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          ptx::sts_v4(lo_base + (ct + (h * 8 + i) * 128) * 16,
-                      __float_as_uint(ptx::tf32_residual(v[i].x)),
+        for (int i = 0; i < 8; ++i) {
+          uint32_t off = (ct + (h * 8 + i) * 128) * 16;
+          if (BB && (h * 8 + i) * 128 < OP_BYTES / 16) {  // chunk lies in the A half
+            // dense [k][m8][b4] A chunk -> 32 B-atom swizzle (k row % 4 XOR granule)
+            off ^= ((off >> 7) & 3u) << 5;
+            ptx::sts_v4(lo_base + 2 * OP_BYTES + off, __float_as_uint(v[i].x),
+                        __float_as_uint(v[i].y), __float_as_uint(v[i].z), __float_as_uint(v[i].w));
+          }
+          ptx::sts_v4(lo_base + off, __float_as_uint(ptx::tf32_residual(v[i].x)),
                       __float_as_uint(ptx::tf32_residual(v[i].y)),
                       __float_as_uint(ptx::tf32_residual(v[i].z)),
                       __float_as_uint(ptx::tf32_residual(v[i].w)));
+        }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -216,18 +256,21 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     const uint32_t empty_leader[2] = {ptx::mapa(&acc_empty[0], 0), ptx::mapa(&acc_empty[1], 0)};
     uint32_t tcount = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-      const Tile tc = tile_of(t, tiles_m, tiles_n, p.batch);
+      const Tile tc = tile_of<BB>(t, tiles_m, tiles_n, nbatch);
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_full[b], ph);
       ptx::tc_fence_after();
 #ifdef SBT_TRACE
-      long long t_ld = 0, t_st = 0, t_begin = clock64();
+      long long t_ld = 0, t_begin = clock64();
 #endif
-      const int64_t row = tc.m0 + rank * HM + warp * 32 + lane;
-      const bool row_ok = row < p.m;
+      const int r = warp * 32 + lane;
+      // BB: MMA row r is (batch entry 4*pb + r%4, m = m0 + 32*rank + r/4)
+      const int64_t row = BB ? tc.m0 + rank * 32 + (r >> 2) : tc.m0 + rank * HM + r;
+      const int64_t bidx = BB ? tc.pb * 4 + (r & 3) : tc.pb;
+      const bool row_ok = row < p.m && (!BB || bidx < p.batch);
       float* __restrict__ crow =
-          p.c + tc.pb * p.cps + tc.qb * p.cps2 + (row_ok ? row : 0) * p.crs;
+          p.c + (row_ok ? bidx * p.cps + row * p.crs : 0) + tc.qb * p.cps2;
       const bool vec = (p.ccs == 1) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                        (tc.n0 + BN <= p.n) && p.beta == 0.f;
       const uint32_t acc_col = SPLIT_ACC ? 0u : b * BN;
@@ -318,10 +361,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         ptx::mbar_wait(&full[s], (it / RAW_SLOTS) & 1u);
         TRACE(3, int(it));
         ptx::tc_fence_after();
-        const uint32_t a_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
-        const uint32_t b_raw = a_raw + OP_BYTES;
-        const uint32_t a_lo = ptx::smem_addr(lo_ring + ls * SLOT_BYTES);
+        const uint32_t b_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES) + OP_BYTES;
+        const uint32_t a_lo = ptx::smem_addr(lo_ring + ls * LO_SLOT_BYTES);
         const uint32_t b_lo = a_lo + OP_BYTES;
+        // BB: A_hi is the converter's swizzled copy, not the dense raw box
+        const uint32_t a_raw = BB ? a_lo + 2 * OP_BYTES : b_raw - OP_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);

@@ -197,6 +197,39 @@ int sbt_probe_fp64_peak(int kind, double* tflops) {
   return check_cuda(cudaGetLastError(), "probe");
 }
 
+// Diagnostics: measured dense TF32 tensor-pipe throughput (tcgen05.mma
+// kind::tf32) in TFLOP/s on the current device; 3xTF32 peak = this / 3.
+int sbt_probe_tf32_peak(double* tflops) {
+  if (!tflops) return fail(SBT_EINVAL, "bad probe arguments");
+  auto kern = probe::tf32_umma_peak_kernel;
+  int rc;
+  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            probe::kTf32ProbeSmem),
+                       "cudaFuncSetAttribute")) != SBT_OK)
+    return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 8192, blocks = kNumSMs;
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {  // first launch warms up; keep the fastest
+    cudaEventRecord(e0);
+    kern<<<blocks, 128, probe::kTf32ProbeSmem>>>(iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  // 4 MMAs of M=128 N=256 K=8 per iteration per CTA
+  const double flops = 2.0 * blocks * double(iters) * 4.0 * 128 * 256 * 8;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  note_launch("probe_tf32_umma");
+  return check_cuda(cudaGetLastError(), "probe");
+}
+
 #define SBT_DEFINE(T, SUF)                                                                     \
   int sbt_gemm_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,     \
                           int64_t ars, int64_t acs, const T* b, int64_t ob, int64_t brs,        \

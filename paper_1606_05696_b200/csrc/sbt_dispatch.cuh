@@ -107,10 +107,10 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   return 0;
 }
 
-template <bool AK, bool BK_, bool SPLIT, int KB>
+template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false>
 static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream) {
-  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB>;
-  constexpr int smem = tf32tma::Geo<KB>::SMEM_BYTES;
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB>;
+  constexpr int smem = tf32tma::Geo<KB, BB>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -121,23 +121,51 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream) {
   const CUtensorMapSwizzle kswz = KB == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUtensorMap ta, tb;
   const bool ok_a =
-      AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, KB, 128,
-                         kswz)
-         : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, KB,
-                         CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      BB ? make_tmap_f32(&ta, p.a, p.batch, p.m, p.ars, p.k, p.acs, p.batch2, p.aps2, 4, 8,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, KB)
+      : AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, KB, 128,
+                           kswz)
+           : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, KB,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const bool ok_b =
       BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB, 128,
                           kswz)
           : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
-  const int64_t tiles_m = ceil_div(p.m, tf32tma::BM), tiles_n = ceil_div(p.n, tf32tma::BN);
-  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  const int64_t tiles_m = ceil_div(p.m, BB ? 64 : tf32tma::BM);
+  const int64_t tiles_n = ceil_div(p.n, tf32tma::BN);
+  const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
   const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
       p, ta, tb, tiles_m, tiles_n, total);
-  note_launch(SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma");
+  note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
+                 : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma"));
   return 1;
+}
+
+// Batch-blocked pair kernel for the exceptional cases: A unit-stride along
+// the batch, B batch-independent (see k_tf32x3_pair_tma.cuh).  Tries the
+// problem as given and transposed; returns 1 if launched, 0 if not eligible.
+template <bool SPLIT>
+static int launch_tf32_bb(const GemmParams<float>& p0, cudaStream_t stream) {
+  static const int kb = env_int("SBT_TC_BK", 32);
+  for (int orient = 0; orient < 2; ++orient) {
+    const GemmParams<float> p = orient ? transposed(p0) : p0;
+    if (p.aps != 1 || p.bps != 0 || p.batch < 2 || !aligned16(p.a)) continue;
+    if (p.ars < 4 || p.acs < 4 || !vmult<float>(p.ars) || !vmult<float>(p.acs) ||
+        !vmult<float>(p.aps2))
+      continue;
+    if (p.m < 64 || p.n < 192) continue;
+    const int bm = b_major(p);
+    if (!bm) continue;
+    if (bm == 1)
+      return kb == 16 ? launch_tf32tma_kb<false, true, SPLIT, 16, true>(p, stream)
+                      : launch_tf32tma_kb<false, true, SPLIT, 32, true>(p, stream);
+    return kb == 16 ? launch_tf32tma_kb<false, false, SPLIT, 16, true>(p, stream)
+                    : launch_tf32tma_kb<false, false, SPLIT, 32, true>(p, stream);
+  }
+  return 0;
 }
 
 template <bool AK, bool BK_, bool SPLIT>
@@ -237,13 +265,19 @@ static int try_tensor_f64(const GemmParams<double>& p0, cudaStream_t stream, boo
 
 // Returns 1 if launched, 0 if not eligible, <0 on error.
 static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
+  static const int variant = env_int("SBT_TC_VARIANT", 0);
+  if (variant == 0 || variant == 5) {
+    static const int split_env = env_int("SBT_TC_SPLITACC", -1);
+    const bool split = split_env < 0 ? (p0.k > 512) : (split_env != 0);
+    const int rc = split ? launch_tf32_bb<true>(p0, stream) : launch_tf32_bb<false>(p0, stream);
+    if (rc != 0) return rc;
+  }
   GemmParams<float> p;
   int am = 0, bm = 0;
   if (!orient(p0, &p, &am, &bm)) return 0;
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
-  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel
-  static const int variant = env_int("SBT_TC_VARIANT", 0);
+  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair
   if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 4) {
     static const int split_env = env_int("SBT_TC_SPLITACC", -1);
     const bool split = split_env < 0 ? (p.k > 512) : (split_env != 0);

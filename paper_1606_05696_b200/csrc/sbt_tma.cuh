@@ -30,10 +30,10 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 4-D fp32 view: dims (d0 contiguous, d1, batch, batch2), element strides
-// (s1, sb, sb2), box (b0, b1, 1, 1).  Returns false if TMA cannot express it.
+// (s1, sb, sb2), box (b0, b1, b2, 1).  Returns false if TMA cannot express it.
 inline bool make_tmap_f32(CUtensorMap* map, const float* base, int64_t d0, int64_t d1,
                           int64_t s1, int64_t batch, int64_t sb, int64_t batch2, int64_t sb2,
-                          uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz) {
+                          uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz, uint32_t b2 = 1) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
   cuuint64_t dims[4] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(sb ? batch : 1),
@@ -44,7 +44,7 @@ inline bool make_tmap_f32(CUtensorMap* map, const float* base, int64_t d0, int64
     if ((strides[i] & 15) || strides[i] >= (cuuint64_t(1) << 40)) return false;
   for (int i = 0; i < 4; ++i)
     if (dims[i] == 0 || dims[i] > (cuuint64_t(1) << 32)) return false;
-  cuuint32_t box[4] = {b0, b1, 1, 1};
+  cuuint32_t box[4] = {b0, b1, b2, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,

@@ -242,6 +242,7 @@ __device__ __forceinline__ void mma2_tf32_ss(uint32_t d_tmem, uint64_t adesc, ui
 //       atoms, 32 B granules XOR (K-row % 4); LBO = stride between MN atoms,
 //       SBO = stride between 4-deep K groups.  (The only MN-major smem layout
 //       UMMA accepts for tf32, cf. CuTe Layout_MN_SW128_32B_Atom.)
+constexpr uint32_t kLayoutInterleave = 0;  // no swizzle: 8 x 16 B core matrices
 constexpr uint32_t kLayoutSW128 = 2;
 constexpr uint32_t kLayoutSW64 = 4;   // K-major 64 B rows, 16 B chunks XOR (row/2)%4
 constexpr uint32_t kLayoutSW128Base32B = 1;

@@ -470,3 +470,64 @@ def test_tensor_paths_are_used_for_the_36_cases():
 def test_fp64_probe_reports_a_plausible_peak():
     tf = _lib.probe_fp64_peak("dmma")
     assert 5.0 < tf < 100.0
+
+
+# ------------------------------------------------------------------ exceptional cases, batch-blocked
+
+
+def _strided_case_run(cid, ext, pad, dtype, seed, alpha=1.0, beta=0.0):
+    """One case with the 3rd-order operand's first mode padded to ``pad``
+    elements (leading dimension > extent): ragged batch groups, non-packed."""
+    rng = np.random.default_rng(seed)
+    case = find_case(2, 3, cid)
+    spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+
+    def lay(labels, padded):
+        dims = [ext[l] for l in labels]
+        strides, s = [], 1
+        for i, d in enumerate(dims):
+            strides.append(s)
+            s *= (pad if (padded and i == 0) else d)
+        return Layout(tuple(dims), tuple(strides))
+
+    la = lay(spec.labels_a, len(spec.labels_a) == 3)
+    lb = lay(spec.labels_b, len(spec.labels_b) == 3)
+    lc = Layout.packed([ext[l] for l in spec.labels_c])
+    ha = rng.uniform(-1, 1, la.min_buffer_len())
+    hb = rng.uniform(-1, 1, lb.min_buffer_len())
+    hc = rng.uniform(-1, 1, lc.size)
+    a, b = DenseTensor(la, dev(ha, dtype)), DenseTensor(lb, dev(hb, dtype))
+    c = DenseTensor(lc, dev(hc, dtype))
+    execute_plan(plan_single_mode(spec, la, lb, lc), a, b, alpha, beta, c)
+    kern = _lib.last_kernel()
+    want = host(dev(hc, dtype)).copy()
+    oplan.contract(spec.labels_a, spec.labels_b, spec.labels_c, ext, host(a.data),
+                   host(b.data), alpha, beta, want, layouts=(la, lb, lc))
+    return naive.max_rel_err(host(c.data), want), kern
+
+
+@pytest.mark.parametrize("cid", sorted(EXCEPTIONAL))
+def test_exceptional_cases_batch_blocked_n256(cid):
+    """fp32 exceptional cases run on the batch-blocked CTA-pair kernel (A's
+    unit-stride batch folded into the MMA rows) and match the oracle."""
+    err = _case_run(cid, 256, torch.float32, seed=7 + hash(cid) % 97, alpha=0.75, beta=0.5)
+    assert err <= TOL[torch.float32], (cid, err)
+    err = _case_run(cid, 256, torch.float32, seed=3)
+    assert _lib.last_kernel().startswith("tc_tf32x3_pair_bb"), (cid, _lib.last_kernel())
+    assert err <= TOL[torch.float32], (cid, err)
+
+
+@pytest.mark.parametrize("cid", ["3.4", "4.6", "5.6", "6.4"])
+def test_exceptional_ragged_batch_groups(cid):
+    """Batch extent not a multiple of 4 (padded leading dimension), ragged
+    m / n / k tails: the batch-blocked tiles must mask rows and zero-fill."""
+    case = find_case(2, 3, cid)
+    third, second = ((case.labels_b, case.labels_a) if len(case.labels_b) == 3
+                     else (case.labels_a, case.labels_b))
+    batch = third[0]                                   # unit-stride (extended) mode
+    free2 = next(l for l in second if l != "k")        # the MMA N extent
+    ext = {l: 200 for l in "mnp"}
+    ext.update({batch: 22, free2: 256, "k": 132})
+    err, kern = _strided_case_run(cid, ext, 24, torch.float32, seed=11, alpha=1.5, beta=-0.5)
+    assert kern.startswith("tc_tf32x3_pair_bb"), (cid, kern)
+    assert err <= TOL[torch.float32], (cid, err, kern)

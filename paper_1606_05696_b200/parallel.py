@@ -120,10 +120,18 @@ def _einsum_local():
     return mode_product, gram
 
 
-def _factor(gram, rank):
-    from .tucker import _sign_fix, jacobi_eigh
-    _, vecs = jacobi_eigh(gram)
-    return _sign_fix(vecs[:, :rank].contiguous())
+def _factor(gram, rank, warm=None, dtype="float64"):
+    """Top-``rank`` sign-fixed eigenvectors of an (all-reduced, hence
+    rank-identical) Gram: the device subspace solver for CUDA Grams, the full
+    eigendecomposition for the CPU (gloo test) path."""
+    from .tucker import _SUBSPACE_TOL, _SUBSPACE_TOL_F32, _sign_fix, jacobi_eigh, top_eigh
+    if gram.is_cuda:
+        tol = _SUBSPACE_TOL if dtype == "float64" else _SUBSPACE_TOL_F32
+        _, vecs, _ = top_eigh(gram, rank, q0=warm, tol=tol)
+    else:
+        _, vecs = jacobi_eigh(gram)
+        vecs = vecs[:, :rank]
+    return _sign_fix(vecs.contiguous())
 
 
 def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e-10,
@@ -145,6 +153,7 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
         raise ValueError(f"rank {rank}: slab shape {tuple(t_local.shape)} != "
                          f"{(d0, d1, c1 - c0)}")
     mode_product, gram = local() if local else _device_local()
+    dt = str(t_local.dtype).replace("torch.", "")
     ranks = tuple(int(r) for r in ranks)
 
     def allreduce(x):
@@ -178,14 +187,14 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
         iters = it + 1
         # skip=0: modes 1 then 2 (contracting the sharded mode: partial sums)
         y = allreduce(mode_product(mode_product(t_local, u[1], 1), u2_local(), 2).contiguous())
-        u[0] = _factor(gram(y, 0), ranks[0])
+        u[0] = _factor(gram(y, 0), ranks[0], u[0], dt)
         x0 = mode_product(t_local, u[0], 0)
         # skip=1: [0, 2] -> partial sums over the sharded mode
         y = allreduce(mode_product(x0, u2_local(), 2).contiguous())
-        u[1] = _factor(gram(y, 1), ranks[1])
+        u[1] = _factor(gram(y, 1), ranks[1], u[1], dt)
         # skip=2: [0, 1] -> mode-2 distributed result
         y2 = allgather_last(mode_product(x0, u[1], 1).contiguous())
-        u[2] = _factor(gram(y2, 2), ranks[2])
+        u[2] = _factor(gram(y2, 2), ranks[2], u[2], dt)
         core = mode_product(y2, u[2], 2)
         g2 = float(torch.sum(core.to(torch.float64) ** 2))
         resid = np.sqrt(max(0.0, norm_t ** 2 - g2))

@@ -63,6 +63,107 @@ def jacobi_eigh(sym, tol: float = 1e-12, max_sweeps: int = 60):
     return w, v
 
 
+# Leading-eigenvector solver for the HOOI Grams.  Only the top ``rank``
+# eigenpairs of an n x n PSD Gram are needed (tucker.py:69-70 keeps the first
+# ``rank`` columns), so for n >= _SUBSPACE_MIN_N the factor comes from block
+# subspace iteration with Rayleigh-Ritz, warm-started from the previous HOOI
+# factor: every n-sized product is an fp64 GEMM on the sm_100a kernels, the
+# (rank+oversample)^2 projected problem is solved on the host, and the loop
+# stops when every kept Ritz pair has ||G u - w u|| <= tol * w_max -- the
+# accuracy of a full eigh.  If it has not converged after _SUBSPACE_MAX_IT
+# sweeps (small eigengap), the full eigendecomposition is used instead.
+_SUBSPACE_MIN_N = 128
+_SUBSPACE_MAX_IT = 40
+_SUBSPACE_TOL = 1e-12
+# fp32 tensors: the Gram of fp32 (3xTF32) products is itself only ~1e-7
+# accurate, so Ritz pairs with residual <= 1e-7 * w_max are at data precision
+_SUBSPACE_TOL_F32 = 1e-7
+SWEEP_LOG = []  # (n, rank, sweep, max relative residual): diagnostics only
+
+
+def _gemm64(opa, opb, m, n, k, a, lda, b, ldb, c, ldc, alpha=1.0, beta=0.0):
+    """fp64 GEMM on the device through the library (column-major flat views)."""
+    gemm(opa, opb, m, n, k, alpha, a.reshape(-1), lda, b.reshape(-1), ldb, beta,
+         c.reshape(-1), ldc)
+
+
+def _orthonormal(z):
+    """Orthonormal basis of the columns of z (n x p, column-major as a (p, n)
+    row-major torch tensor): Householder QR (cuSOLVER)."""
+    torch = _torch()
+    q, _ = torch.linalg.qr(z.t())
+    return q.t().contiguous()
+
+
+def top_eigh(g, rank: int, q0=None, tol: float = _SUBSPACE_TOL,
+             max_iter: int = _SUBSPACE_MAX_IT):
+    """Top ``rank`` eigenpairs (descending) of the symmetric PSD matrix ``g``
+    (torch fp64, n x n, on the device).  Returns (w[rank], V[n, rank]) and the
+    number of subspace sweeps (0 = full eigh was used)."""
+    torch = _torch()
+    n = g.shape[0]
+    if n < _SUBSPACE_MIN_N or 4 * rank > n:
+        w, v = jacobi_eigh(g)
+        return w[:rank], v[:, :rank], 0
+    p_full = min(n, rank + max(8, rank // 2))
+    gen = torch.Generator(device=g.device).manual_seed(20260824 + n * 131 + rank)
+    # bases are stored transposed: qt[p, n] row-major == Q[n, p] column-major
+    if q0 is not None:
+        # warm start: the previous (orthonormal) factor alone; oversampling
+        # columns are added only if one sweep does not converge
+        qt = torch.as_tensor(q0, dtype=torch.float64, device=g.device).t().contiguous()
+        expand = True
+    else:
+        qt = _orthonormal(torch.randn(p_full, n, device=g.device, dtype=torch.float64,
+                                      generator=gen))
+        expand = False
+    gm = g.contiguous()  # symmetric: row-major == column-major
+    wmax = None
+    prev_res = None
+    for it in range(1, max_iter + 1):
+        p = qt.shape[0]
+        zt = torch.empty_like(qt)
+        h = torch.empty(p, p, device=g.device, dtype=torch.float64)
+        _gemm64(Op.Normal, Op.Normal, n, p, n, gm, n, qt, n, zt, n)          # Z = G Q
+        _gemm64(Op.Transpose, Op.Normal, p, p, n, qt, n, zt, n, h, p)        # H = Q^T Z
+        hh = h.cpu().numpy()
+        w, v = np.linalg.eigh(0.5 * (hh + hh.T))
+        order = np.argsort(w)[::-1]
+        w, v = w[order], v[:, order]
+        vt = torch.as_tensor(np.ascontiguousarray(v), device=g.device)
+        ut = torch.empty_like(qt)
+        yt = torch.empty_like(qt)
+        _gemm64(Op.Normal, Op.Normal, n, p, p, qt, n, vt.t().contiguous(), p, ut, n)  # U = Q V
+        _gemm64(Op.Normal, Op.Normal, n, p, p, zt, n, vt.t().contiguous(), p, yt, n)  # Y = G U
+        wt = torch.as_tensor(w[:rank].copy(), device=g.device)
+        res = torch.linalg.vector_norm(yt[:rank] - wt[:, None] * ut[:rank], dim=1)
+        wmax = max(float(w[0]), 0.0)
+        if wmax == 0.0:
+            break
+        rmax = float(res.max())
+        SWEEP_LOG.append((n, rank, it, rmax / wmax))
+        if rmax <= tol * wmax:
+            return (wt, ut[:rank].t().contiguous(), it)
+        # give up early when the observed contraction rate cannot reach tol in
+        # a few more sweeps (small eigengap): the full solver is cheaper then
+        if prev_res is not None and it >= 3:
+            rate = rmax / prev_res
+            need = np.log(tol * wmax / rmax) / np.log(rate) if 0 < rate < 1 else np.inf
+            if need > 6:
+                break
+        prev_res = rmax
+        if expand and p < p_full:
+            extra = torch.randn(p_full - p, n, device=g.device, dtype=torch.float64,
+                                generator=gen)
+            qt = _orthonormal(torch.cat([yt, extra]))
+            prev_res = None
+        else:
+            qt = _orthonormal(yt)
+        expand = False
+    w, v = jacobi_eigh(g)
+    return w[:rank], v[:, :rank], 0
+
+
 def _sign_fix(u):
     """Largest-magnitude entry of each column made positive (tucker.py:71-75)."""
     torch = _torch()
@@ -74,25 +175,41 @@ def _sign_fix(u):
 
 def gram_of_unfolding(t: DenseTensor, r: int):
     """fp64 Gram matrix Y_(r) Y_(r)^T of the mode-r unfolding, on the device.
-    Mode 0 and the last mode are read in place by one GEMM launch; middle
-    modes go through a packed unfolding copy first."""
+
+    The Gram does not depend on the order of the unfolding's columns, so any
+    buffer with mode r as its unit-stride mode serves.  An fp64 packed tensor
+    is read in place for mode 0 and the last mode (one GEMM launch); otherwise
+    one fused pass converts to fp64 AND moves mode r to the front (the copy
+    the fp32 -> fp64 conversion needs anyway), then one GEMM."""
     torch = _torch()
     dims = t.layout.dims
     rows = dims[r]
-    src = t
-    if t.dtype != torch.float64:
-        src = DenseTensor(t.layout, t.data.to(torch.float64))
-    g = torch.empty(rows * rows, dtype=torch.float64, device=t.device)
     cols = int(np.prod(dims)) // rows
-    if t.layout.is_packed() and r == 0:
-        gemm(Op.Normal, Op.Transpose, rows, rows, cols, 1.0, src.data, rows, src.data, rows,
-             0.0, g, rows)
-    elif t.layout.is_packed() and r == len(dims) - 1:
-        gemm(Op.Transpose, Op.Normal, rows, rows, cols, 1.0, src.data, cols, src.data, cols,
-             0.0, g, rows)
+    g = torch.empty(rows * rows, dtype=torch.float64, device=t.device)
+    if r in (0, len(dims) - 1):
+        if t.dtype == torch.float64 and t.layout.is_packed():
+            src = t.data
+        else:                                            # one pass: convert / pack
+            x = t.view()
+            rev = tuple(reversed(range(x.dim())))
+            buf = torch.empty(tuple(x.shape[i] for i in rev), dtype=torch.float64,
+                              device=t.device)
+            buf.copy_(x.permute(rev))
+            src = buf.reshape(-1)
+        if r == 0:
+            gemm(Op.Normal, Op.Transpose, rows, rows, cols, 1.0, src, rows, src, rows,
+                 0.0, g, rows)
+        else:
+            gemm(Op.Transpose, Op.Normal, rows, rows, cols, 1.0, src, cols, src, cols,
+                 0.0, g, rows)
     else:
-        u = unfold(src, r)
-        gemm(Op.Normal, Op.Transpose, rows, rows, cols, 1.0, u.data, rows, u.data, rows,
+        x = t.view().movedim(r, 0)                       # logical (rows, rest...)
+        rev = tuple(reversed(range(x.dim())))
+        buf = torch.empty(tuple(x.shape[i] for i in rev), dtype=torch.float64,
+                          device=t.device)
+        buf.copy_(x.permute(rev))                         # column-major, mode r fastest
+        flat = buf.reshape(-1)
+        gemm(Op.Normal, Op.Transpose, rows, rows, cols, 1.0, flat, rows, flat, rows,
              0.0, g, rows)
     return g.reshape(rows, rows).t()  # column-major -> logical (symmetric anyway)
 
@@ -110,11 +227,16 @@ def leading_left_singular_vectors(mat, rank: int):
     return u.cpu().numpy() if is_np else u
 
 
-def _factor_from_tensor(t: DenseTensor, r: int, rank: int):
+def _factor_from_tensor(t: DenseTensor, r: int, rank: int, warm=None):
+    """Leading ``rank`` left singular vectors of the mode-r unfolding: top
+    eigenvectors of its fp64 Gram (subspace iteration warm-started from the
+    previous factor ``warm`` when given), sign-fixed as tucker.py:71-75."""
     if rank > t.layout.dims[r]:
         raise ValueError(f"rank {rank} exceeds row count {t.layout.dims[r]}")
-    _, vecs = jacobi_eigh(gram_of_unfolding(t, r))
-    return _sign_fix(vecs[:, :rank].contiguous())
+    torch = _torch()
+    tol = _SUBSPACE_TOL if t.dtype == torch.float64 else _SUBSPACE_TOL_F32
+    _, vecs, _ = top_eigh(gram_of_unfolding(t, r), rank, q0=warm, tol=tol)
+    return _sign_fix(vecs.contiguous())
 
 
 def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
@@ -213,9 +335,7 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
         if not 1 <= rank <= dim:
             raise ValueError(f"rank {rank} invalid for mode {r} extent {dim}")
     torch = _torch()
-    t64 = t if t.dtype == torch.float64 else DenseTensor(t.layout, t.data.to(torch.float64))
-    factors = [_factor_from_tensor(t64, r, ranks[r]) for r in range(order)]
-    del t64
+    factors = [_factor_from_tensor(t, r, ranks[r]) for r in range(order)]
     norm_t = _norm(t)
     fits = []
     prev = -np.inf
@@ -226,13 +346,13 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
         if fast:
             # skip=0 chain: modes 1, 2 (reference order); then X0 = T x_0 U_0^T
             y = _mode_product_chain(t, factors, skip=0, transpose=True)
-            factors[0] = _factor_from_tensor(y, 0, ranks[0])
+            factors[0] = _factor_from_tensor(y, 0, ranks[0], warm=factors[0])
             x0 = _mode_product(t, factors[0], 0, True)
             # reference skip=1 chain is [0, 2] and skip=2 chain is [0, 1]
             y = _mode_product(x0, factors[2], 2, True)
-            factors[1] = _factor_from_tensor(y, 1, ranks[1])
+            factors[1] = _factor_from_tensor(y, 1, ranks[1], warm=factors[1])
             y2 = _mode_product(x0, factors[1], 1, True)
-            factors[2] = _factor_from_tensor(y2, 2, ranks[2])
+            factors[2] = _factor_from_tensor(y2, 2, ranks[2], warm=factors[2])
             # reference core chain: mode 0, then the larger of modes 1 / 2 first
             if t.layout.dims[1] >= t.layout.dims[2]:
                 core = _mode_product(y2, factors[2], 2, True)
@@ -241,7 +361,7 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
         else:
             for r in range(order):
                 y = _mode_product_chain(t, factors, skip=r, transpose=True)
-                factors[r] = _factor_from_tensor(y, r, ranks[r])
+                factors[r] = _factor_from_tensor(y, r, ranks[r], warm=factors[r])
             core = tucker_core(t, factors)
         norm_g = _norm(core)
         resid = np.sqrt(max(0.0, norm_t ** 2 - norm_g ** 2))

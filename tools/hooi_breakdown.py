@@ -39,3 +39,6 @@ timed("hooi 3 iters", lambda: sbt.hooi(t, (r, r, r), max_iters=3, tol=-1.0), rep
 from paper_1606_05696_b200 import _lib
 print("tf32 UMMA peak TFLOP/s:", [round(_lib.probe_tf32_peak(), 1) for _ in range(3)])
 print("dmma peak TFLOP/s:", round(_lib.probe_fp64_peak("dmma"), 2))
+tk.SWEEP_LOG.clear()
+sbt.hooi(t, (r, r, r), max_iters=3, tol=-1.0)
+print("sweep log:", [(a, c, f"{d:.1e}") for a, b, c, d in tk.SWEEP_LOG])

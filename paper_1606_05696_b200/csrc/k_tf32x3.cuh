@@ -51,7 +51,11 @@ struct Cfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int A_VEC = BM * BK / 4 / kProducers;  // float4 per producer thread
   static constexpr int B_VEC = BN * BK / 4 / kProducers;
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  // main (hi*hi) accumulator + a separate one for the two small cross terms
+  // (the tensor core truncates the fp32 accumulator on every MMA; keeping the
+  // 2^-11-sized terms apart roughly halves that error, cf. k_tf32x3_pair_tma)
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
 };
 
 // Byte offset of element (mn, k) inside a [rows x 32] K-major SW128 tile.
@@ -215,9 +219,10 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
         const uint64_t dbh = ptx::umma_desc(b_hi + j * b_step, b_lbo, b_sbo, b_lay);
         const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
         const uint32_t acc = (kb | j) ? 1u : 0u;
-        ptx::mma_tf32_ss(tmem_base, dal, dbh, idesc, acc);  // small terms first
-        ptx::mma_tf32_ss(tmem_base, dah, dbl, idesc, 1u);
-        ptx::mma_tf32_ss(tmem_base, dah, dbh, idesc, 1u);
+        const uint32_t small = tmem_base + C_::ACC_COLS;
+        ptx::mma_tf32_ss(small, dal, dbh, idesc, acc);  // small terms apart
+        ptx::mma_tf32_ss(small, dah, dbl, idesc, 1u);
+        ptx::mma_tf32_ss(tmem_base, dah, dbh, idesc, acc);
       }
       ptx::tc_commit(&empty[s]);  // stage reusable once these MMAs retire
     }
@@ -236,14 +241,18 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
     float* crow = Cp + row * p.crs;
 #pragma unroll 1
     for (int cc = 0; cc < HALF; cc += 16) {
-      uint32_t r[16];
-      ptx::tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(col0 + cc), r);
+      uint32_t r[16], q[16];
+      const uint32_t ta = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(col0 + cc);
+      ptx::tmem_ld16(ta, r);
+      ptx::tmem_ld16(ta + C_::ACC_COLS, q);
       ptx::tmem_ld_wait();
       if (row_ok) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int64_t col = n0 + col0 + cc + j;
-          if (col < p.n) store_out(crow + col * p.ccs, __uint_as_float(r[j]), p.alpha, p.beta);
+          if (col < p.n)
+            store_out(crow + col * p.ccs, __uint_as_float(r[j]) + __uint_as_float(q[j]), p.alpha,
+                      p.beta);
         }
       }
     }

@@ -365,6 +365,8 @@ __global__ void reduce_splits_kernel(const T* __restrict__ w, int64_t nsplit, in
 
 template <typename T>
 static int launch_gemm_core(const GemmParams<T>& p, cudaStream_t stream);
+template <typename T>
+static int launch_chunked(const GemmParams<T>& p, cudaStream_t stream);
 
 template <typename T>
 static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
@@ -388,13 +390,13 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
   q.k = kc; q.batch = S - 1;             // full chunks
   q.aps = kc * p.acs; q.bps = kc * p.brs;
   int rc = 0;
-  if (q.batch > 0) rc = launch_gemm_core<T>(q, stream);
+  if (q.batch > 0) rc = launch_chunked<T>(q, stream);
   if (rc == 0) {                          // ragged last chunk
     GemmParams<T> t = q;
     t.batch = 1; t.k = p.k - (S - 1) * kc;
     t.a = p.a + (S - 1) * kc * p.acs; t.b = p.b + (S - 1) * kc * p.brs;
     t.c = w + (S - 1) * p.m * p.n;
-    rc = launch_gemm_core<T>(t, stream);
+    rc = launch_chunked<T>(t, stream);
   }
   if (rc == 0) {
     const int64_t total = p.m * p.n;
@@ -407,6 +409,36 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
   return rc < 0 ? rc : 1;
 }
 
+// fp32 accuracy guard for long reductions.  The tensor core truncates its fp32
+// accumulator on every MMA, a bias that grows linearly with K (measured 3xTF32
+// max_rel_err with the split small-term accumulator: 3.3e-6 at K=1024, 6.8e-6
+// at K=2048, 1.1e-5 at K=4096).  Longer reductions run as K-chunks of at most
+// kMaxChunkK, the first with the caller's beta, the rest accumulating into C
+// (beta = 1): the cross-chunk sums are round-to-nearest fp32 adds, so the error
+// stays at the K = kMaxChunkK level for any K.
+constexpr int64_t kMaxChunkK = 2048;
+
+template <typename T>
+static int launch_chunked(const GemmParams<T>& p, cudaStream_t stream) {
+  if constexpr (sizeof(T) == 4) {
+    if (p.k > kMaxChunkK) {
+      const int64_t nch = ceil_div(p.k, kMaxChunkK);
+      const int64_t kc = ceil_div(ceil_div(p.k, nch), 32) * 32;  // keep 16 B alignment
+      for (int64_t k0 = 0; k0 < p.k; k0 += kc) {
+        GemmParams<T> q = p;
+        q.k = (p.k - k0) < kc ? (p.k - k0) : kc;
+        q.a = p.a + k0 * p.acs;
+        q.b = p.b + k0 * p.brs;
+        if (k0 > 0) q.beta = T(1);
+        const int rc = launch_gemm_core<T>(q, stream);
+        if (rc != 0) return rc;
+      }
+      return 0;
+    }
+  }
+  return launch_gemm_core<T>(p, stream);
+}
+
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
   if (kernel_override() == 0) {
@@ -414,7 +446,7 @@ static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
     if (rc < 0) return rc;
     if (rc == 1) return 0;
   }
-  return launch_gemm_core<T>(p, stream);
+  return launch_chunked<T>(p, stream);
 }
 
 template <typename T>

@@ -595,3 +595,20 @@ def test_hooi_subspace_path_matches_oracle():
             u = model.factors[r].cpu().numpy()
             ur = ref["factors"][r]
             np.testing.assert_allclose(u, ur, atol=utol)
+
+
+@pytest.mark.parametrize("m,n,k,P", [(256, 256, 8192, 2), (128, 128, 40000, 1), (512, 320, 3000, 3)])
+def test_fp32_long_reductions_stay_within_tolerance(m, n, k, P):
+    """3xTF32 truncation bias grows with K; long reductions are K-chunked (and
+    split-K partials too) so max_rel_err stays <= 1e-5 at any K."""
+    rng = np.random.default_rng(k)
+    ha, hb = rng.uniform(-1, 1, m * k * P), rng.uniform(-1, 1, k * n * P)
+    a, b = dev(ha, torch.float32), dev(hb, torch.float32)
+    c = torch.zeros(m * n * P, dtype=torch.float32, device="cuda")
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.0, a, m, m * k, b, k, k * n, 0.0, c, m,
+                                 m * n, P)
+    A = host(a).reshape(P, k, m).transpose(0, 2, 1)
+    B = host(b).reshape(P, n, k).transpose(0, 2, 1)
+    want = np.einsum("pik,pkj->pij", A, B)
+    got = host(c).reshape(P, n, m).transpose(0, 2, 1)
+    assert naive.max_rel_err(got, want) <= TOL[torch.float32]

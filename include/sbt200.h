@@ -56,6 +56,8 @@ int sbt_probe_fp64_peak(int kind, double* tflops);
 /* Diagnostics: measured dense TF32 tensor-pipe throughput (tcgen05.mma
    kind::tf32, TFLOP/s); the 3xTF32 fp32 roofline is this / 3. */
 int sbt_probe_tf32_peak(double* tflops);
+/* The same probe run back to back for `seconds` (clocks under the power cap). */
+int sbt_probe_tf32_sustained(double seconds, double* tflops);
 
 /* ---- reference: _loops_numba.py:12-25 gemm_core (called by kernels.gemm, kernels.py:107) */
 int sbt_gemm_core_f64(int64_t m, int64_t n, int64_t k, double alpha,

@@ -45,6 +45,7 @@ SIGNATURES = {
     "sbt_set_kernel_override": ([c_int], c_int),
     "sbt_probe_fp64_peak": ([c_int, ctypes.POINTER(c_double)], c_int),
     "sbt_probe_tf32_peak": ([ctypes.POINTER(c_double)], c_int),
+    "sbt_probe_tf32_sustained": ([c_double, ctypes.POINTER(c_double)], c_int),
     "sbt_gemm_core_f64": (_core_sig(c_double), c_int),
     "sbt_gemm_core_f32": (_core_sig(c_float), c_int),
     "sbt_batched_core_f64": (_batched_sig(c_double), c_int),
@@ -122,4 +123,12 @@ def probe_tf32_peak() -> float:
     """Measured dense TF32 TFLOP/s of the tcgen05 tensor pipe (3xTF32 peak = / 3)."""
     out = c_double(0.0)
     check(load().sbt_probe_tf32_peak(ctypes.byref(out)), "sbt_probe_tf32_peak")
+    return out.value
+
+
+def probe_tf32_sustained(seconds: float = 3.0) -> float:
+    """Dense TF32 TFLOP/s of the tcgen05 pipe under sustained load (power cap)."""
+    out = c_double(0.0)
+    check(load().sbt_probe_tf32_sustained(float(seconds), ctypes.byref(out)),
+          "sbt_probe_tf32_sustained")
     return out.value

@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters) 
 // three of these MMAs per output product).  One CTA per SM; one thread issues
 // back-to-back tcgen05.mma.cta_group::1.kind::tf32 M=128 N=256 K=8 from a
 // zeroed K-major SW128 tile pair (A 128x32, B 256x32 fp32) into one TMEM
-// accumulator, then waits for the last one to retire.
+// accumulator, then waits for the last one to retire.  Operands are
+// pseudo-random (a zero tile draws less power and would overstate the
+// sustained clock).
 constexpr int kTf32ProbeSmem = (128 + 256) * 128 + 1024 + 64;
 __global__ void __launch_bounds__(128, 1) tf32_umma_peak_kernel(int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -53,8 +55,15 @@ __global__ void __launch_bounds__(128, 1) tf32_umma_peak_kernel(int iters) {
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (128 + 256) * 128);
   uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
-  for (int i = threadIdx.x; i < (128 + 256) * 128 / 16; i += blockDim.x)
-    ptx::sts_v4(ptx::smem_addr(smem) + i * 16, 0u, 0u, 0u, 0u);
+  // pseudo-random operands in [-1, 1): zeros would under-state the power
+  // draw (and so the clock) of a real contraction
+  for (int i = threadIdx.x; i < (128 + 256) * 128 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t(i) + 0x9E3779B9u * (blockIdx.x + 1)) * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<float*>(smem)[i] = float(int32_t(h)) * (1.0f / 2147483648.0f);
+  }
   ptx::fence_proxy_async_smem();
   if (threadIdx.x < 32) ptx::tmem_alloc(slot, 256);
   if (threadIdx.x == 0) {

@@ -230,6 +230,38 @@ int sbt_probe_tf32_peak(double* tflops) {
   return check_cuda(cudaGetLastError(), "probe");
 }
 
+// Sustained variant: back-to-back probe launches for `seconds` (clocks settle
+// under the power cap), throughput of the second half.
+int sbt_probe_tf32_sustained(double seconds, double* tflops) {
+  if (!tflops || !(seconds > 0.0) || seconds > 60.0)
+    return fail(SBT_EINVAL, "bad probe arguments");
+  auto kern = probe::tf32_umma_peak_kernel;
+  int rc;
+  if ((rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            probe::kTf32ProbeSmem),
+                       "cudaFuncSetAttribute")) != SBT_OK)
+    return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 8192, blocks = kNumSMs;
+  const double flops_per_launch = 2.0 * blocks * double(iters) * 4.0 * 128 * 256 * 8;
+  // one launch is ~3 ms at full clock: size the two halves from that
+  const int half = int(seconds / 2 / 3e-3) + 1;
+  for (int i = 0; i < half; ++i) kern<<<blocks, 128, probe::kTf32ProbeSmem>>>(iters);
+  cudaEventRecord(e0);
+  for (int i = 0; i < half; ++i) kern<<<blocks, 128, probe::kTf32ProbeSmem>>>(iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *tflops = flops_per_launch * half / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  note_launch("probe_tf32_umma");
+  return check_cuda(cudaGetLastError(), "probe");
+}
+
 #define SBT_DEFINE(T, SUF)                                                                     \
   int sbt_gemm_core_##SUF(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_t oa,     \
                           int64_t ars, int64_t acs, const T* b, int64_t ob, int64_t brs,        \

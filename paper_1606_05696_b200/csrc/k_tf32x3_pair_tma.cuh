@@ -89,6 +89,19 @@ __device__ long long g_trace_epi[2][64][4];
 struct Tile {
   int64_t m0, n0, pb, qb;
 };
+// Batch folding: a batch mode that only one operand (and C) depends on can be
+// folded into that operand's MMA dimension when the dimension is a multiple of
+// the CTA block (128): M' = m x batch_X rows, row r' = (r' % m, x = r' / m),
+// each CTA's 128 rows inside one x.  This turns e.g. the 4th-order contraction
+// C[mnpq] = A[mkp] B[nkq] (m = n = 128, two batch modes: the planner's
+// LoopStep fused as batch2) into one 16384 x 16384 x 128 GEMM of full 256x256
+// tiles instead of 16384 half-empty 128x128 ones.
+struct Fold {
+  int64_t m_in, n_in;  // inner extents (p.m, p.n)
+  int64_t mtot, ntot;  // folded extents M', N'
+  int fm, fn;          // 0 = none, 1 = folds `batch`, 2 = folds `batch2`
+};
+
 // BB tiles cover 64 m (32 per CTA) x 4 batch entries; pb is then the batch group
 template <bool BB = false>
 __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tiles_n,
@@ -124,10 +137,11 @@ template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
-                       int64_t tiles_n, int64_t total) {
+                       int64_t tiles_n, int64_t total, Fold f) {
   static_assert(!(BB && A_K), "batch-blocked A is MN-major");
-  // number of batch units the tile index runs over (BB: groups of 4 entries)
-  const int64_t nbatch = BB ? (p.batch + 3) / 4 : p.batch;
+  // number of batch units the tile index runs over (BB: groups of 4 entries;
+  // a folded batch mode is not a tile dimension)
+  const int64_t nbatch = BB ? (p.batch + 3) / 4 : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
   using Gm = Geo<BK, BB>;
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
@@ -198,11 +212,25 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           for (int c = 0; c < 4; ++c)
             ptx::tma_load_4d(st + c * (BK * 128), &tmA, &raw_full[s], int(tc.pb * 4),
                              int(tc.m0 + rank * 32 + 8 * c), int(k0), a_bc2 ? 0 : int(tc.qb));
-        } else
-          tma_operand<A_K, BK>(&tmA, st, &raw_full[s], tc.m0 + rank * HM, k0, tc.pb, tc.qb, a_bc,
-                               a_bc2);
-        tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
-                         tc.qb, b_bc, b_bc2);
+          tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
+                               tc.qb, b_bc, b_bc2);
+        } else {
+          // (un)fold: CTA row / column block -> (inner index, folded batch index)
+          int64_t am = tc.m0 + rank * HM, ab = tc.pb, ab2 = tc.qb;
+          if (f.fm) {
+            const int64_t x = am / f.m_in;
+            am -= x * f.m_in;
+            if (f.fm == 1) ab = x; else ab2 = x;
+          }
+          int64_t bn = tc.n0 + rank * HN, bb = tc.pb, bb2 = tc.qb;
+          if (f.fn) {
+            const int64_t y = bn / f.n_in;
+            bn -= y * f.n_in;
+            if (f.fn == 1) bb = y; else bb2 = y;
+          }
+          tma_operand<A_K, BK>(&tmA, st, &raw_full[s], am, k0, ab, ab2, a_bc, a_bc2);
+          tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], bn, k0, bb, bb2, b_bc, b_bc2);
+        }
       }
     }
   } else if (warp >= 4 && warp < 4 + kConvWarps) {
@@ -265,16 +293,22 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       long long t_ld = 0, t_begin = clock64();
 #endif
       const int r = warp * 32 + lane;
-      // BB: MMA row r is (batch entry 4*pb + r%4, m = m0 + 32*rank + r/4)
-      const int64_t row = BB ? tc.m0 + rank * 32 + (r >> 2) : tc.m0 + rank * HM + r;
-      const int64_t bidx = BB ? tc.pb * 4 + (r & 3) : tc.pb;
-      const bool row_ok = row < p.m && (!BB || bidx < p.batch);
+      // BB: MMA row r is (batch entry 4*pb + r%4, m = m0 + 32*rank + r/4);
+      // fold: row r' = m0 + 128*rank + r of M' is (m = r' % m_in, x = r' / m_in)
+      int64_t row = BB ? tc.m0 + rank * 32 + (r >> 2) : tc.m0 + rank * HM + r;
+      int64_t bidx = BB ? tc.pb * 4 + (r & 3) : tc.pb, qidx = tc.qb;
+      bool row_ok = BB ? (row < p.m && bidx < p.batch) : row < f.mtot;
+      if (!BB && f.fm) {
+        const int64_t x = row / f.m_in;
+        row -= x * f.m_in;
+        if (f.fm == 1) bidx = x; else qidx = x;
+      }
       float* __restrict__ crow =
-          p.c + (row_ok ? bidx * p.cps + row * p.crs : 0) + tc.qb * p.cps2;
-      const bool vec = (p.ccs == 1) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
-                       (tc.n0 + BN <= p.n) && p.beta == 0.f;
+          p.c + (row_ok ? bidx * p.cps + row * p.crs + qidx * p.cps2 : 0);
+      const int64_t ncols = BB ? p.n : f.ntot;
+      const bool full_tile = (tc.n0 + BN <= ncols) && p.beta == 0.f;
+      const bool vec = (p.ccs == 1) && full_tile;
       const uint32_t acc_col = SPLIT_ACC ? 0u : b * BN;
-      const bool full_tile = (tc.n0 + BN <= p.n) && p.beta == 0.f;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 16) {
         uint32_t v[16];
@@ -299,22 +333,28 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         t_ld += t1 - t0;
 #endif
         if (!row_ok) continue;
-        if (vec) {
+        // column chunk base: fold keeps a 16-column chunk inside one y (16 | n_in)
+        int64_t col0 = tc.n0 + cc, ycol = 0;
+        if (!BB && f.fn) {
+          const int64_t y = col0 / f.n_in;
+          col0 -= y * f.n_in;
+          ycol = y * (f.fn == 1 ? p.cps : p.cps2);
+        }
+        float* dst = crow + ycol + col0 * p.ccs;
+        if (vec && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(crow + tc.n0 + cc + j) =
+            *reinterpret_cast<float4*>(dst + j) =
                 make_float4(p.alpha * o[j], p.alpha * o[j + 1], p.alpha * o[j + 2],
                             p.alpha * o[j + 3]);
         } else if (full_tile) {
           // interior tile, beta == 0: straight-line stores, one address add each
-          float* dst = crow + (tc.n0 + cc) * p.ccs;
 #pragma unroll
           for (int j = 0; j < 16; ++j) dst[j * p.ccs] = p.alpha * o[j];
         } else {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int64_t col = tc.n0 + cc + j;
-            if (col < p.n) store_out(crow + col * p.ccs, o[j], p.alpha, p.beta);
+            if (tc.n0 + cc + j < ncols) store_out(dst + j * p.ccs, o[j], p.alpha, p.beta);
           }
         }
       }

@@ -107,8 +107,37 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   return 0;
 }
 
+// Fold a batch mode into M (only A and C depend on it) and / or into N (only B
+// and C) when the extent is a multiple of the CTA block but not of the 256-wide
+// pair tile (see k_tf32x3_pair_tma.cuh, struct Fold).
+static tf32tma::Fold make_fold(const GemmParams<float>& p) {
+  tf32tma::Fold f{p.m, p.n, p.m, p.n, 0, 0};
+  auto cnt = [&](int w) { return w == 1 ? p.batch : p.batch2; };
+  auto as = [&](int w) { return w == 1 ? p.aps : p.aps2; };
+  auto bs = [&](int w) { return w == 1 ? p.bps : p.bps2; };
+  if (p.m % tf32tma::BM != 0 && p.m % tf32tma::HM == 0) {
+    for (int w : {2, 1})
+      if (cnt(w) > 1 && bs(w) == 0 && as(w) > 0 && vmult<float>(as(w))) {
+        f.fm = w;
+        f.mtot = p.m * cnt(w);
+        break;
+      }
+  }
+  if (p.n % tf32tma::BN != 0 && p.n % tf32tma::HN == 0) {
+    for (int w : {1, 2})
+      if (w != f.fm && cnt(w) > 1 && as(w) == 0 && bs(w) > 0 && vmult<float>(bs(w))) {
+        f.fn = w;
+        f.ntot = p.n * cnt(w);
+        break;
+      }
+  }
+  return f;
+}
+
 template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false>
-static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream) {
+static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
+                             tf32tma::Fold f = tf32tma::Fold{0, 0, 0, 0, 0, 0}) {
+  if (f.mtot == 0) f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0};
   auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB>;
   constexpr int smem = tf32tma::Geo<KB, BB>::SMEM_BYTES;
   static bool attr_set = false;
@@ -133,13 +162,16 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream) {
           : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
-  const int64_t tiles_m = ceil_div(p.m, BB ? 64 : tf32tma::BM);
-  const int64_t tiles_n = ceil_div(p.n, tf32tma::BN);
-  const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
+  const int64_t tiles_m = ceil_div(f.mtot, BB ? 64 : tf32tma::BM);
+  const int64_t tiles_n = ceil_div(f.ntot, tf32tma::BN);
+  const int64_t nb = BB ? ceil_div(p.batch, 4) : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
+  const int64_t nb2 = (f.fm == 2 || f.fn == 2) ? 1 : p.batch2;
+  const int64_t total = tiles_m * tiles_n * nb * nb2;
   const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
-      p, ta, tb, tiles_m, tiles_n, total);
+      p, ta, tb, tiles_m, tiles_n, total, f);
   note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
+                 : (f.fm || f.fn) ? (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold")
                  : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma"));
   return 1;
 }
@@ -169,18 +201,20 @@ static int launch_tf32_bb(const GemmParams<float>& p0, cudaStream_t stream) {
 }
 
 template <bool AK, bool BK_, bool SPLIT>
-static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream) {
+static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream,
+                              const tf32tma::Fold& f) {
   static const int kb = env_int("SBT_TC_BK", 32);
-  return kb == 16 ? launch_tf32tma_kb<AK, BK_, SPLIT, 16>(p, stream)
-                  : launch_tf32tma_kb<AK, BK_, SPLIT, 32>(p, stream);
+  return kb == 16 ? launch_tf32tma_kb<AK, BK_, SPLIT, 16>(p, stream, f)
+                  : launch_tf32tma_kb<AK, BK_, SPLIT, 32>(p, stream, f);
 }
 
 template <bool SPLIT>
-static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
-  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT>(p, s);
-  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT>(p, s);
-  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT>(p, s);
-  return launch_tf32tma_cfg<false, false, SPLIT>(p, s);
+static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
+                          const tf32tma::Fold& f) {
+  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT>(p, s, f);
+  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT>(p, s, f);
+  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT>(p, s, f);
+  return launch_tf32tma_cfg<false, false, SPLIT>(p, s, f);
 }
 
 template <int BN>
@@ -277,12 +311,15 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
   if (!orient(p0, &p, &am, &bm)) return 0;
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
-  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair
-  if ((variant == 0 && p.n >= 192 && p.m >= 256) || variant == 4) {
+  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair,
+  // 6 = auto without batch folding
+  const tf32tma::Fold fold = variant == 6 ? tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0} : make_fold(p);
+  if (((variant == 0 || variant == 6) && fold.ntot >= 192 && fold.mtot >= 256) ||
+      variant == 4) {
     static const int split_env = env_int("SBT_TC_SPLITACC", -1);
     const bool split = split_env < 0 ? (p.k > 512) : (split_env != 0);
-    const int rc = split ? launch_tf32tma<true>(p, am, bm, stream)
-                         : launch_tf32tma<false>(p, am, bm, stream);
+    const int rc = split ? launch_tf32tma<true>(p, am, bm, stream, fold)
+                         : launch_tf32tma<false>(p, am, bm, stream, fold);
     if (rc != 0) return rc;
   }
   int bn = env_int("SBT_TC_BN", 0);

@@ -612,3 +612,60 @@ def test_fp32_long_reductions_stay_within_tolerance(m, n, k, P):
     want = np.einsum("pik,pkj->pij", A, B)
     got = host(c).reshape(P, n, m).transpose(0, 2, 1)
     assert naive.max_rel_err(got, want) <= TOL[torch.float32]
+
+
+# ------------------------------------------------------------------ batch folding (pair kernel)
+
+
+def test_fourth_order_n128_folds_both_batch_modes():
+    """C[mnpq] = A[mkp] B[nkq] at n=128 (BASELINE configs[4]): one launch of
+    the CTA-pair kernel with p folded into M and q into N; sampled (p, q)
+    slices against fp64 matmuls."""
+    n = 128
+    rng = np.random.default_rng(44)
+    spec = ContractionSpec(tuple("mkp"), tuple("nkq"), tuple("mnpq"))
+    la, lb, lc = Layout.packed((n,) * 3), Layout.packed((n,) * 3), Layout.packed((n,) * 4)
+    ha, hb = rng.uniform(-1, 1, la.size), rng.uniform(-1, 1, lb.size)
+    a = DenseTensor(la, dev(ha, torch.float32))
+    b = DenseTensor(lb, dev(hb, torch.float32))
+    c = DenseTensor(lc, torch.full((lc.size,), float("nan"), dtype=torch.float32, device="cuda"))
+    n0 = _lib.launch_count()
+    execute_plan(plan_single_mode(spec, la, lb, lc), a, b, 1.0, 0.0, c)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() - n0 == 1
+    assert _lib.last_kernel().startswith("tc_tf32x3_pair_fold"), _lib.last_kernel()
+    A = host(a.data).reshape(n, n, n)     # [p][k][m]
+    B = host(b.data).reshape(n, n, n)     # [q][k][n]
+    C = c.data.view(n, n, n, n)           # [q][p][n][m]
+    for (p, q) in [(0, 0), (127, 127), (5, 77), (64, 3), (100, 126)] + \
+            [tuple(x) for x in rng.integers(0, n, (8, 2))]:
+        want = (A[p].T @ B[q])            # [m][n]
+        got = C[q, p].double().cpu().numpy().T
+        assert naive.max_rel_err(got, want) <= TOL[torch.float32], (p, q)
+    assert not torch.isnan(C).any()
+
+
+@pytest.mark.parametrize("shape", [
+    # m, n, k, batch, aps, bps : fold batch into M (B broadcast) / into N (A broadcast)
+    (384, 256, 96, 5, "a", 0),
+    (256, 384, 200, 3, 0, "b"),
+    (640, 256, 64, 4, "a", 0),
+])
+def test_batch_fold_into_m_or_n(shape):
+    m, n, k, P, aps, bps = shape
+    rng = np.random.default_rng(m + n + k)
+    aps = m * k if aps == "a" else 0
+    bps = k * n if bps == "b" else 0
+    ha = rng.uniform(-1, 1, m * k * (P if aps else 1))
+    hb = rng.uniform(-1, 1, k * n * (P if bps else 1))
+    hc = rng.uniform(-1, 1, m * n * P)
+    a, b, c = dev(ha, torch.float32), dev(hb, torch.float32), dev(hc, torch.float32)
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.5, a, m, aps, b, k, bps, -0.25, c, m,
+                                 m * n, P)
+    kern = _lib.last_kernel()
+    want = host(dev(hc, torch.float32)).copy()
+    oapi.run_call("strided_batched_gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=1.5,
+                  lda=m, loa=aps, ldb=k, lob=bps, beta=-0.25, ldc=m, loc=m * n, batch_count=P),
+                  host(a), host(b), want)
+    assert kern.startswith("tc_tf32x3_pair_fold"), kern
+    assert naive.max_rel_err(host(c), want) <= TOL[torch.float32]

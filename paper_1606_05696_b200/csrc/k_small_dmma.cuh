@@ -1,0 +1,149 @@
+// K3 (fp64, 16 < n <= 32): small-matrix batched GEMM on the DMMA pipe.
+//
+// The SIMT K3 kernel (k_small.cuh) reaches 0.93-0.95 of HBM bandwidth for fp64
+// n <= 16, but at n = 32 (AI = 2.7 flop/B) it is shared-memory bound: a 4x4
+// register block reads 4 bytes of shared memory per DFMA.  Here each warp owns
+// one matrix and runs the whole 32x32x32 product as 128 DMMA.8x8x4 with every
+// fragment loaded once per k-step (0.5 B of shared memory per FMA).
+//
+// Operand staging: one 3-D TMA box per operand per group of G matrices,
+// (rows, cols, G) with the row extent padded to LD = rows + 4 doubles.  The
+// TMA zero-fills the out-of-range rows, so the box lands as [matrix][col][LD]
+// with a column stride of LD (== 4 mod 16 doubles): the DMMA fragment loads
+// (8 rows x 4 columns per half-warp) hit 16 distinct bank pairs -- no
+// conflicts, no padding copy.
+//
+// The product is computed transposed, C^T = B^T A^T (MMA M = C column j, MMA
+// N = C row i), so each thread's accumulator pair is two consecutive rows of a
+// column of C: one 16-byte store.
+//
+// Requires A stored with rows contiguous (ars = 1, acs = m), B with k
+// contiguous (brs = 1, bcs = k), C dense (crs = 1, ccs = m); m, n multiples of
+// 8 and <= 32, k a multiple of 4 and <= 32 (checked by the dispatcher).
+#pragma once
+#include <cuda.h>
+
+#include "sbt_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace sbt {
+namespace small_dmma {
+
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;
+constexpr int G = 4;        // matrices per group (one per warp)
+constexpr int STAGES = 3;
+constexpr int LD_MAX = 36;  // padded leading dimension for extents <= 32
+
+__host__ __device__ constexpr int ld_of(int rows) { return ((rows + 15) / 16) * 16 + 4; }
+__host__ __device__ constexpr int stage_doubles() { return G * 2 * LD_MAX * 32; }
+constexpr int SMEM_BYTES = STAGES * stage_doubles() * 8 + 64;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(ptx::smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(ptx::smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+small_dmma_kernel(GemmParams<double> p, const __grid_constant__ CUtensorMap tmA,
+                  const __grid_constant__ CUtensorMap tmB, int64_t ngroups) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * stage_doubles() * 8);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = int(p.m), n = int(p.n), k = int(p.k);
+  const int lda = ld_of(m), ldb = ld_of(k);
+  const int a_doubles = lda * k, b_doubles = ldb * n;  // one matrix, padded
+  const uint32_t tx = uint32_t(G * (a_doubles + b_doubles) * 8);
+
+  auto issue = [&](int64_t grp, int slot) {
+    double* sa = sm + slot * stage_doubles();
+    double* sb = sa + G * a_doubles;
+    ptx::mbar_arrive_expect_tx(&full[slot], tx);
+    tma_load_3d(sa, &tmA, &full[slot], 0, 0, int(grp * G));
+    tma_load_3d(sb, &tmB, &full[slot], 0, 0, int(grp * G));
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbarrier_init();
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t gi = blockIdx.x + int64_t(s) * gridDim.x;
+      if (gi < ngroups) issue(gi, s);
+    }
+  }
+  __syncthreads();
+
+  const int mt = m >> 3, nt = n >> 3;      // C row / column tiles of 8
+  const int r4 = lane & 3, q8 = lane >> 2;  // fragment coordinates
+  const bool vec = p.beta == 0.0 && (p.ccs % 2 == 0) && (p.cps % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(p.c) & 15) == 0);
+  uint32_t it = 0;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    const int slot = int(it % STAGES);
+    ptx::mbar_wait(&full[slot], (it / STAGES) & 1u);
+    const int64_t bidx = grp * G + warp;
+    if (bidx < p.batch) {
+      const double* sa = sm + slot * stage_doubles() + warp * a_doubles;
+      const double* sb = sm + slot * stage_doubles() + G * a_doubles + warp * b_doubles;
+      double acc[4][4][2];  // [j tile][i tile][pair]
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) acc[jt][i2][0] = acc[jt][i2][1] = 0.0;
+      for (int l0 = 0; l0 < k; l0 += 4) {
+        double fa[4], fb[4];
+        // MMA A = B^T (8 j x 4 l): thread (j = q8, l = r4) -> B[l + j*ldb]
+        // MMA B = A^T (4 l x 8 i): thread (l = r4, i = q8) -> A[i + l*lda]
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+          fa[jt] = jt < nt ? sb[(l0 + r4) + (8 * jt + q8) * ldb] : 0.0;
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2)
+          fb[i2] = i2 < mt ? sa[(8 * i2 + q8) + (l0 + r4) * lda] : 0.0;
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int i2 = 0; i2 < 4; ++i2)
+            if (jt < nt && i2 < mt) dmma(acc[jt][i2], fa[jt], fb[i2]);
+      }
+      // D[j][i] (j = 8 jt + q8, i = 8 i2 + 2 r4 + {0,1}) = C[i + j*ccs]
+      double* C = p.c + bidx * p.cps;
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
+          if (jt >= nt || i2 >= mt) continue;
+          double* dst = C + (8 * i2 + 2 * r4) + int64_t(8 * jt + q8) * p.ccs;
+          if (vec) {
+            *reinterpret_cast<double2*>(dst) =
+                make_double2(p.alpha * acc[jt][i2][0], p.alpha * acc[jt][i2][1]);
+          } else {
+            store_out(dst, acc[jt][i2][0], p.alpha, p.beta);
+            store_out(dst + 1, acc[jt][i2][1], p.alpha, p.beta);
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with this slot
+    const int64_t gnext = grp + int64_t(STAGES) * gridDim.x;
+    if (tid == 0 && gnext < ngroups) issue(gnext, slot);
+  }
+}
+
+}  // namespace small_dmma
+}  // namespace sbt

@@ -18,6 +18,7 @@
 #include "k_tf32x3_pair_tma.cuh"
 #include "k_dmma.cuh"
 #include "k_small.cuh"
+#include "k_small_dmma.cuh"
 #include "sbt_tma.cuh"
 
 namespace sbt {
@@ -363,6 +364,35 @@ static int launch_small_s(const GemmParams<T>& p, bool am, bool bk, cudaStream_t
   return launch_small_cfg<T, S, false, false>(p, s);
 }
 
+// fp64 16 < n <= 32 with column-major A, B and C: the DMMA variant of K3.
+static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
+  using namespace small_dmma;
+  if (p.m % 8 || p.n % 8 || p.k % 4 || p.m > 32 || p.n > 32 || p.k > 32) return 0;
+  if (!(p.ars == 1 && p.acs == p.m && p.brs == 1 && p.bcs == p.k && p.crs == 1 && p.ccs == p.m))
+    return 0;
+  if (p.aps % 2 || p.bps % 2 || p.aps < p.m * p.k || p.bps < p.k * p.n) return 0;
+  if (!aligned16(p.a) || !aligned16(p.b) || p.batch > (int64_t(1) << 31)) return 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(small_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_tmap_f64_3d(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, ld_of(int(p.m)),
+                        uint32_t(p.k), G) ||
+      !make_tmap_f64_3d(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, ld_of(int(p.k)),
+                        uint32_t(p.n), G))
+    return 0;
+  const int64_t ngroups = ceil_div(p.batch, G);
+  const int64_t grid = ngroups < int64_t(kNumSMs) ? ngroups : int64_t(kNumSMs);
+  small_dmma_kernel<<<dim3(unsigned(grid)), dim3(kThreads), SMEM_BYTES, stream>>>(p, ta, tb,
+                                                                                 ngroups);
+  note_launch("small_batched_dmma_f64");
+  return 1;
+}
+
 // Many tiny dense matrices: every extent <= 64, each matrix stored densely.
 template <typename T>
 static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
@@ -375,6 +405,13 @@ static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
   if (!vmult<T>(p.m * p.k) || !vmult<T>(p.k * p.n) || !vmult<T>(p.aps) || !vmult<T>(p.bps) ||
       !aligned16(p.a) || !aligned16(p.b))
     return 0;
+  if constexpr (sizeof(T) == 8) {
+    static const int use_dmma = env_int("SBT_SMALL_DMMA", 1);
+    if (use_dmma && mx > 16 && mx <= 32) {
+      const int rc = try_small_dmma(p, stream);
+      if (rc != 0) return rc;
+    }
+  }
   if (mx <= 8) return launch_small_s<T, 8>(p, am, bk, stream);
   if (mx <= 16) return launch_small_s<T, 16>(p, am, bk, stream);
   if (mx <= 32) return launch_small_s<T, 32>(p, am, bk, stream);

@@ -52,4 +52,25 @@ inline bool make_tmap_f32(CUtensorMap* map, const float* base, int64_t d0, int64
   return r == CUDA_SUCCESS;
 }
 
+// 3-D fp64 view for the batched small-matrix DMMA kernel: dims (d0 contiguous,
+// d1, batch) with element strides (s1, sb), box (b0, b1, b2).  b0 may exceed
+// d0: the TMA zero-fills the extra rows, which pads the smem leading dimension.
+inline bool make_tmap_f64_3d(CUtensorMap* map, const double* base, int64_t d0, int64_t d1,
+                             int64_t s1, int64_t batch, int64_t sb, uint32_t b0, uint32_t b1,
+                             uint32_t b2) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(batch)};
+  cuuint64_t strides[2] = {cuuint64_t(s1) * 8, cuuint64_t(sb) * 8};
+  for (int i = 0; i < 2; ++i)
+    if ((strides[i] & 15) || strides[i] == 0 || strides[i] >= (cuuint64_t(1) << 40)) return false;
+  if (b0 > 256 || b1 > 256 || b2 > 256) return false;
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace sbt

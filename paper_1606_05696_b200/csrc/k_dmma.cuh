@@ -23,13 +23,29 @@ constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
 constexpr int kThreads = 256;
 constexpr int LDK = 20;   // [mn][k] rows (16 k + 4 pad)
 constexpr int LDMN = 132; // [k][mn] rows (128 mn + 4 pad)
+// Batch-blocked A (the exceptional cases: A unit-stride along the batch, B
+// batch-independent): the tile's 128 MMA rows are 4 batch entries x 32 m,
+// MMA row R = 32 b + m.  A is staged with 8-byte cp.async, lanes walking the
+// batch fastest (coalesced: 4 entries = one 32 B sector), into [k][LDBB] rows
+// with smem position 36 b + m -- 2 wavefronts per warp store (the minimum for
+// 8 B x 32 lanes) and, with LDBB = 148 = 4 mod 16, conflict-free fragment
+// loads.  A fragment (8 consecutive R) is 8 consecutive m of one batch entry,
+// so the epilogue stores 64-byte runs of C exactly as for plain tiles.
+constexpr int LDBB = 148;
 constexpr int TILE_DOUBLES = 128 * LDK > 16 * LDMN ? 128 * LDK : 16 * LDMN;  // 2560 vs 2112
+static_assert(16 * LDBB <= TILE_DOUBLES, "BB tile fits the stage");
 constexpr int SMEM_BYTES = STAGES * 2 * TILE_DOUBLES * 8;                   // 120 KB
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   const int bytes = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -68,7 +84,21 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
   }
 }
 
-template <bool A_K, bool B_K>
+// BB A staging: 128 rows (4 batch x 32 m) x 16 k, 8-byte chunks
+__device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__ src, int64_t b0,
+                                         int64_t m0, int64_t k0, int64_t nbatch, int64_t m_ext,
+                                         int64_t k_ext, int64_t ars, int64_t acs, int tid) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = tid + i * kThreads;
+    const int k = e >> 7, b = e & 3, m = (e >> 2) & 31;
+    const int64_t gb = b0 + b, gm = m0 + m, gk = k0 + k;
+    const bool ok = gb < nbatch && gm < m_ext && gk < k_ext;
+    cp_async8(dst + k * LDBB + 36 * b + m, ok ? src + gb + gm * ars + gk * acs : src, ok);
+  }
+}
+
+template <bool A_K, bool B_K, bool BB = false>
 __global__ void __launch_bounds__(kThreads, 1)
 dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   extern __shared__ __align__(16) double sm[];
@@ -77,20 +107,24 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
 
   int64_t t = blockIdx.x;
-  const int64_t m0 = (t % tiles_m) * BM;
+  const int64_t m0 = (t % tiles_m) * (BB ? 32 : BM);
   t /= tiles_m;
   const int64_t n0 = (t % tiles_n) * BN;
   t /= tiles_n;
-  const int64_t pb = t % p.batch, qb = t / p.batch;
-  const double* __restrict__ A = p.a + pb * p.aps + qb * p.aps2;
-  const double* __restrict__ B = p.b + pb * p.bps + qb * p.bps2;
+  const int64_t nbatch = BB ? (p.batch + 3) / 4 : p.batch;
+  const int64_t pb = t % nbatch, qb = t / nbatch;
+  const double* __restrict__ A = p.a + (BB ? 0 : pb * p.aps) + qb * p.aps2;
+  const double* __restrict__ B = p.b + (BB ? 0 : pb * p.bps) + qb * p.bps2;
   const int nkb = int((p.k + BK - 1) / BK);
 
   auto stage = [&](int kb) {
     double* sa = sm + (kb % STAGES) * 2 * TILE_DOUBLES;
     double* sb = sa + TILE_DOUBLES;
     const int64_t k0 = int64_t(kb) * BK;
-    stage_operand<A_K>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
+    if (BB)
+      stage_bb(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
+    else
+      stage_operand<A_K>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
     stage_operand<B_K>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
   };
 
@@ -119,7 +153,8 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int m = wm * 64 + i * 8 + fr;
-        af[i] = A_K ? sa[m * LDK + kk + fk] : sa[(kk + fk) * LDMN + m];
+        if (BB) af[i] = sa[(kk + fk) * LDBB + 36 * (m >> 5) + (m & 31)];
+        else af[i] = A_K ? sa[m * LDK + kk + fk] : sa[(kk + fk) * LDMN + m];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -134,17 +169,20 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   }
   cp_async_wait<0>();
 
-  double* C = p.c + pb * p.cps + qb * p.cps2;
+  double* C = p.c + (BB ? 0 : pb * p.cps) + qb * p.cps2;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + wm * 64 + i * 8 + fr;
+    const int R = wm * 64 + i * 8 + fr;
+    const int64_t row = BB ? m0 + (R & 31) : m0 + R;
     if (row >= p.m) continue;
+    if (BB && pb * 4 + (R >> 5) >= p.batch) continue;
+    double* Cr = BB ? C + (pb * 4 + (R >> 5)) * p.cps : C;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t col = n0 + wn * 32 + j * 8 + 2 * fk + h;
-        if (col < p.n) store_out(C + row * p.crs + col * p.ccs, acc[i][j][h], p.alpha, p.beta);
+        if (col < p.n) store_out(Cr + row * p.crs + col * p.ccs, acc[i][j][h], p.alpha, p.beta);
       }
     }
   }

@@ -267,9 +267,9 @@ static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm
   return true;
 }
 
-template <bool AK, bool BK_>
+template <bool AK, bool BK_, bool BB = false>
 static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
-  auto kern = dmma::dmma_gemm_kernel<AK, BK_>;
+  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -277,16 +277,35 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
       return -3;
     attr_set = true;
   }
-  const int64_t tiles_m = ceil_div(p.m, dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
-  const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
+  const int64_t tiles_m = ceil_div(p.m, BB ? 32 : dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
+  const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
   kern<<<dim3(unsigned(total)), dim3(dmma::kThreads), dmma::SMEM_BYTES, stream>>>(p, tiles_m,
                                                                                 tiles_n);
-  note_launch("tc_dmma_f64");
+  note_launch(BB ? "tc_dmma_f64_bb" : "tc_dmma_f64");
   return 1;
 }
 
+// fp64 exceptional cases: batch-blocked DMMA tiles (k_dmma.cuh), as given or
+// transposed.  Returns 1 if launched, 0 if not eligible.
+static int try_dmma_bb(const GemmParams<double>& p0, cudaStream_t stream) {
+  for (int orient = 0; orient < 2; ++orient) {
+    const GemmParams<double> p = orient ? transposed(p0) : p0;
+    if (p.aps != 1 || p.bps != 0 || p.batch < 4 || p.m < 16 || p.n < 64) continue;
+    const int bm = b_major(p);
+    if (!bm) continue;
+    return bm == 1 ? launch_dmma_cfg<false, true, true>(p, stream)
+                   : launch_dmma_cfg<false, false, true>(p, stream);
+  }
+  return 0;
+}
+
 static int try_tensor_f64(const GemmParams<double>& p0, cudaStream_t stream, bool forced) {
+  static const int use_bb = env_int("SBT_DMMA_BB", 1);
+  if (use_bb) {
+    const int rc = try_dmma_bb(p0, stream);
+    if (rc != 0) return rc;
+  }
   GemmParams<double> p;
   int am = 0, bm = 0;
   if (!orient(p0, &p, &am, &bm)) return 0;

@@ -507,6 +507,14 @@ def _strided_case_run(cid, ext, pad, dtype, seed, alpha=1.0, beta=0.0):
 
 
 @pytest.mark.parametrize("cid", sorted(EXCEPTIONAL))
+def test_exceptional_cases_batch_blocked_f64_n256(cid):
+    """fp64 exceptional cases on the batch-blocked DMMA tiles."""
+    err = _case_run(cid, 256, torch.float64, seed=5 + hash(cid) % 89, alpha=-1.25, beta=0.5)
+    assert _lib.last_kernel() == "tc_dmma_f64_bb", (cid, _lib.last_kernel())
+    assert err <= TOL[torch.float64], (cid, err)
+
+
+@pytest.mark.parametrize("cid", sorted(EXCEPTIONAL))
 def test_exceptional_cases_batch_blocked_n256(cid):
     """fp32 exceptional cases run on the batch-blocked CTA-pair kernel (A's
     unit-stride batch folded into the MMA rows) and match the oracle."""
@@ -517,8 +525,9 @@ def test_exceptional_cases_batch_blocked_n256(cid):
     assert err <= TOL[torch.float32], (cid, err)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("cid", ["3.4", "4.6", "5.6", "6.4"])
-def test_exceptional_ragged_batch_groups(cid):
+def test_exceptional_ragged_batch_groups(cid, dtype):
     """Batch extent not a multiple of 4 (padded leading dimension), ragged
     m / n / k tails: the batch-blocked tiles must mask rows and zero-fill."""
     case = find_case(2, 3, cid)
@@ -528,9 +537,10 @@ def test_exceptional_ragged_batch_groups(cid):
     free2 = next(l for l in second if l != "k")        # the MMA N extent
     ext = {l: 200 for l in "mnp"}
     ext.update({batch: 22, free2: 256, "k": 132})
-    err, kern = _strided_case_run(cid, ext, 24, torch.float32, seed=11, alpha=1.5, beta=-0.5)
-    assert kern.startswith("tc_tf32x3_pair_bb"), (cid, kern)
-    assert err <= TOL[torch.float32], (cid, err, kern)
+    err, kern = _strided_case_run(cid, ext, 24, dtype, seed=11, alpha=1.5, beta=-0.5)
+    want_kern = "tc_tf32x3_pair_bb" if dtype == torch.float32 else "tc_dmma_f64_bb"
+    assert kern.startswith(want_kern), (cid, kern)
+    assert err <= TOL[dtype], (cid, err, kern)
 
 
 # ------------------------------------------------------------------ HOOI eigensolver (subspace)

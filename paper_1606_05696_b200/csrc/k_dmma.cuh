@@ -20,7 +20,11 @@ namespace sbt {
 namespace dmma {
 
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;      // staging loops assume >= 256 threads
+template <int NW>
+struct WarpGrid {                    // NW = 8: 2 x 4 warps of 64 x 32; 16: 4 x 4 of 32 x 32
+  static constexpr int WM = NW / 4, TM = 128 / WM / 8;  // warp rows, DMMA tiles per warp row
+};
 constexpr int LDK = 20;   // [mn][k] rows (16 k + 4 pad)
 constexpr int LDMN = 132; // [k][mn] rows (128 mn + 4 pad)
 // Batch-blocked A (the exceptional cases: A unit-stride along the batch, B
@@ -63,13 +67,13 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // Stage one operand tile (rows = MN extent 128, k = 16) with 16-byte cp.async.
 // KMAJ: global k unit-stride -> smem [mn][LDK]; else mn unit-stride -> [k][LDMN].
-template <bool KMAJ>
+template <bool KMAJ, int NT = kThreads>
 __device__ __forceinline__ void stage_operand(double* dst, const double* __restrict__ src,
                                               int64_t mn0, int64_t k0, int64_t mn_ext,
                                               int64_t k_ext, int64_t s_mn, int64_t s_k, int tid) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {  // 1024 chunks of 2 doubles
-    const int e = tid + i * kThreads;
+  for (int i = 0; i < 1024 / NT; ++i) {  // 1024 chunks of 2 doubles
+    const int e = tid + i * NT;
     if (KMAJ) {
       const int mn = e >> 3, k2 = (e & 7) * 2;
       const int64_t gm = mn0 + mn, gk = k0 + k2;
@@ -85,12 +89,13 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
 }
 
 // BB A staging: 128 rows (4 batch x 32 m) x 16 k, 8-byte chunks
+template <int NT = kThreads>
 __device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__ src, int64_t b0,
                                          int64_t m0, int64_t k0, int64_t nbatch, int64_t m_ext,
                                          int64_t k_ext, int64_t ars, int64_t acs, int tid) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int e = tid + i * kThreads;
+  for (int i = 0; i < 2048 / NT; ++i) {
+    const int e = tid + i * NT;
     const int k = e >> 7, b = e & 3, m = (e >> 2) & 31;
     const int64_t gb = b0 + b, gm = m0 + m, gk = k0 + k;
     const bool ok = gb < nbatch && gm < m_ext && gk < k_ext;
@@ -98,13 +103,14 @@ __device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__
   }
 }
 
-template <bool A_K, bool B_K, bool BB = false>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool A_K, bool B_K, bool BB = false, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 1)
 dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   extern __shared__ __align__(16) double sm[];
+  constexpr int NT = NW * 32, WM = WarpGrid<NW>::WM, TM = WarpGrid<NW>::TM;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
+  const int wm = warp % WM, wn = warp / WM;  // WM x 4 warps
 
   int64_t t = blockIdx.x;
   const int64_t m0 = (t % tiles_m) * (BB ? 32 : BM);
@@ -122,15 +128,15 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
     double* sb = sa + TILE_DOUBLES;
     const int64_t k0 = int64_t(kb) * BK;
     if (BB)
-      stage_bb(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
+      stage_bb<NT>(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
     else
-      stage_operand<A_K>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
-    stage_operand<B_K>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
+      stage_operand<A_K, NT>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
+    stage_operand<B_K, NT>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
   };
 
-  double acc[8][4][2];
+  double acc[TM][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -149,10 +155,10 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
     const double* sb = sa + TILE_DOUBLES;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[8], bf[4];
+      double af[TM], bf[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = wm * 64 + i * 8 + fr;
+      for (int i = 0; i < TM; ++i) {
+        const int m = wm * (TM * 8) + i * 8 + fr;
         if (BB) af[i] = sa[(kk + fk) * LDBB + 36 * (m >> 5) + (m & 31)];
         else af[i] = A_K ? sa[m * LDK + kk + fk] : sa[(kk + fk) * LDMN + m];
       }
@@ -162,7 +168,7 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
         bf[j] = B_K ? sb[n * LDK + kk + fk] : sb[(kk + fk) * LDMN + n];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
@@ -171,8 +177,8 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
 
   double* C = p.c + (BB ? 0 : pb * p.cps) + qb * p.cps2;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int R = wm * 64 + i * 8 + fr;
+  for (int i = 0; i < TM; ++i) {
+    const int R = wm * (TM * 8) + i * 8 + fr;
     const int64_t row = BB ? m0 + (R & 31) : m0 + R;
     if (row >= p.m) continue;
     if (BB && pb * 4 + (R >> 5) >= p.batch) continue;

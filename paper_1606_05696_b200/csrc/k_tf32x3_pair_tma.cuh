@@ -45,6 +45,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "sbt_common.cuh"
 #include "sm100_ptx.cuh"
 
@@ -119,17 +121,21 @@ __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tile
 // TMA loads of one operand half (128 rows/cols of the MMA dimension x BK k).
 // K-major: one box (BK k, 128 mn).  MN-major: four boxes (32 mn, BK k), one per
 // 32-wide MN atom column, each a contiguous slab of BK 128-byte rows.
-template <bool KMAJ, int BK>
+// PREFETCH: the same boxes as L2 prefetches (no smem destination).
+template <bool KMAJ, int BK, bool PREFETCH = false>
 __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar,
                                             int64_t mn0, int64_t k0, int64_t b, int64_t b2,
                                             bool bcast, bool bcast2) {
   const int cb = bcast ? 0 : int(b), cb2 = bcast2 ? 0 : int(b2);
   if (KMAJ) {
-    ptx::tma_load_4d(dst, tm, bar, int(k0), int(mn0), cb, cb2);
+    if (PREFETCH) ptx::tma_prefetch_4d(tm, int(k0), int(mn0), cb, cb2);
+    else ptx::tma_load_4d(dst, tm, bar, int(k0), int(mn0), cb, cb2);
   } else {
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      ptx::tma_load_4d(dst + c * (BK * 128), tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
+    for (int c = 0; c < 4; ++c) {
+      if (PREFETCH) ptx::tma_prefetch_4d(tm, int(mn0 + 32 * c), int(k0), cb, cb2);
+      else ptx::tma_load_4d(dst + c * (BK * 128), tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
+    }
   }
 }
 
@@ -137,7 +143,7 @@ template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
-                       int64_t tiles_n, int64_t total, Fold f) {
+                       int64_t tiles_n, int64_t total, Fold f, int p_prefetch) {
   static_assert(!(BB && A_K), "batch-blocked A is MN-major");
   // number of batch units the tile index runs over (BB: groups of 4 entries;
   // a folded batch mode is not a tile dimension)
@@ -199,37 +205,82 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     if (lane == 0) {
       // -------------------------------------------------------- TMA producer
       const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
-      for (int64_t g = 0; g < n_iter; ++g) {
-        const uint32_t s = uint32_t(g % RAW_SLOTS);
-        ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
-        TRACE(0, int(g));
-        const Tile tc = tile_of<BB>(pair + (g / nkb) * npairs, tiles_m, tiles_n, nbatch);
-        const int64_t k0 = int64_t(g % nkb) * BK;
-        uint8_t* st = raw_ring + s * SLOT_BYTES;
-        ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
+      // Per-tile TMA coordinates, decoded once per tile (64-bit divisions are
+      // slow on the single producer thread)
+      struct Coord {
+        int am, ab, ab2, bn, bb, bb2;
+      };
+      auto decode = [&](int64_t tile_idx) {
+        const Tile tc = tile_of<BB>(tile_idx, tiles_m, tiles_n, nbatch);
+        Coord c;
+        if (BB) {
+          c.am = int(tc.m0 + rank * 32); c.ab = int(tc.pb * 4); c.ab2 = a_bc2 ? 0 : int(tc.qb);
+          c.bn = int(tc.n0 + rank * HN); c.bb = b_bc ? 0 : int(tc.pb); c.bb2 = b_bc2 ? 0 : int(tc.qb);
+          return c;
+        }
+        // (un)fold: CTA row / column block -> (inner index, folded batch index)
+        int64_t am = tc.m0 + rank * HM, ab = tc.pb, ab2 = tc.qb;
+        if (f.fm) {
+          const int64_t x = am / f.m_in;
+          am -= x * f.m_in;
+          if (f.fm == 1) ab = x; else ab2 = x;
+        }
+        int64_t bn = tc.n0 + rank * HN, bb = tc.pb, bb2 = tc.qb;
+        if (f.fn) {
+          const int64_t y = bn / f.n_in;
+          bn -= y * f.n_in;
+          if (f.fn == 1) bb = y; else bb2 = y;
+        }
+        c.am = int(am); c.ab = a_bc ? 0 : int(ab); c.ab2 = a_bc2 ? 0 : int(ab2);
+        c.bn = int(bn); c.bb = b_bc ? 0 : int(bb); c.bb2 = b_bc2 ? 0 : int(bb2);
+        return c;
+      };
+      // issue the TMA boxes of one K-block: into raw slot st (PF = false) or
+      // as L2 prefetches (PF = true, st unused)
+      auto boxes = [&](const Coord& c, int k0, uint8_t* st, uint64_t* bar, auto pf) {
+        constexpr bool PF = decltype(pf)::value;
         if (BB) {  // four dense (4 batch, 8 m, BK k) boxes [k][m8][b4], one per MN atom
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            ptx::tma_load_4d(st + c * (BK * 128), &tmA, &raw_full[s], int(tc.pb * 4),
-                             int(tc.m0 + rank * 32 + 8 * c), int(k0), a_bc2 ? 0 : int(tc.qb));
-          tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], tc.n0 + rank * HN, k0, tc.pb,
-                               tc.qb, b_bc, b_bc2);
+          for (int q = 0; q < 4; ++q) {
+            if (PF) ptx::tma_prefetch_4d(&tmA, c.ab, c.am + 8 * q, k0, c.ab2);
+            else ptx::tma_load_4d(st + q * (BK * 128), &tmA, bar, c.ab, c.am + 8 * q, k0, c.ab2);
+          }
         } else {
-          // (un)fold: CTA row / column block -> (inner index, folded batch index)
-          int64_t am = tc.m0 + rank * HM, ab = tc.pb, ab2 = tc.qb;
-          if (f.fm) {
-            const int64_t x = am / f.m_in;
-            am -= x * f.m_in;
-            if (f.fm == 1) ab = x; else ab2 = x;
+          tma_operand<A_K, BK, PF>(&tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
+        }
+        tma_operand<B_K, BK, PF>(&tmB, st + OP_BYTES, bar, c.bn, k0, c.bb, c.bb2, false, false);
+      };
+      // L2 prefetch distance (K-blocks ahead of the smem ring)
+      const int pfd = p_prefetch & 0xff;
+      const bool dbg_no_tma = (p_prefetch >> 8) & 1;  // diagnostics: MMA/convert loop only
+      int64_t pf_tile = pair;       // prefetch cursor (tile, k-block)
+      int pf_kb = 0;
+      Coord pf_c = decode(pf_tile);
+      auto prefetch_next = [&]() {
+        if (pf_tile >= total) return;
+        boxes(pf_c, pf_kb * BK, nullptr, nullptr, std::true_type{});
+        if (++pf_kb == nkb) {
+          pf_kb = 0;
+          pf_tile += npairs;
+          if (pf_tile < total) pf_c = decode(pf_tile);
+        }
+      };
+      for (int i = 0; i < pfd; ++i) prefetch_next();
+      int64_t g = 0;
+      for (int64_t t = pair; t < total; t += npairs) {
+        const Coord c = decode(t);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const uint32_t s = uint32_t(g % RAW_SLOTS);
+          ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
+          TRACE(0, int(g));
+          if (pfd > 0) prefetch_next();
+          uint8_t* st = raw_ring + s * SLOT_BYTES;
+          if (dbg_no_tma) {
+            ptx::mbar_arrive(&raw_full[s]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
+            boxes(c, kb * BK, st, &raw_full[s], std::false_type{});
           }
-          int64_t bn = tc.n0 + rank * HN, bb = tc.pb, bb2 = tc.qb;
-          if (f.fn) {
-            const int64_t y = bn / f.n_in;
-            bn -= y * f.n_in;
-            if (f.fn == 1) bb = y; else bb2 = y;
-          }
-          tma_operand<A_K, BK>(&tmA, st, &raw_full[s], am, k0, ab, ab2, a_bc, a_bc2);
-          tma_operand<B_K, BK>(&tmB, st + OP_BYTES, &raw_full[s], bn, k0, bb, bb2, b_bc, b_bc2);
         }
       }
     }
@@ -251,7 +302,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
       constexpr int NV = 2 * Gm::VEC;  // float4 chunks per thread (A and B halves)
 #pragma unroll
-      for (int h = 0; h < NV / 8; ++h) {
+      for (int h = 0; h < ((p_prefetch >> 9) & 1 ? 0 : NV / 8); ++h) {
         float4 v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 8 + i) * 128) * 16);

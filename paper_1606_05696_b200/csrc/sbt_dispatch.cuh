@@ -169,8 +169,11 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
   const int64_t nb2 = (f.fm == 2 || f.fn == 2) ? 1 : p.batch2;
   const int64_t total = tiles_m * tiles_n * nb * nb2;
   const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
+  // low byte: L2 prefetch distance (measured: no gain, 0); bits 8/9: diagnostics
+  // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
+  static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8);
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
-      p, ta, tb, tiles_m, tiles_n, total, f);
+      p, ta, tb, tiles_m, tiles_n, total, f, prefetch);
   note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
                  : (f.fm || f.fn) ? (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold")
                  : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma"));
@@ -267,9 +270,9 @@ static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm
   return true;
 }
 
-template <bool AK, bool BK_, bool BB = false>
-static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
-  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB>;
+template <bool AK, bool BK_, bool BB, int NW>
+static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
+  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -280,10 +283,16 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   const int64_t tiles_m = ceil_div(p.m, BB ? 32 : dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
   const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
-  kern<<<dim3(unsigned(total)), dim3(dmma::kThreads), dmma::SMEM_BYTES, stream>>>(p, tiles_m,
-                                                                                tiles_n);
+  kern<<<dim3(unsigned(total)), dim3(NW * 32), dmma::SMEM_BYTES, stream>>>(p, tiles_m, tiles_n);
   note_launch(BB ? "tc_dmma_f64_bb" : "tc_dmma_f64");
   return 1;
+}
+
+template <bool AK, bool BK_, bool BB = false>
+static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
+  static const int nw = env_int("SBT_DMMA_WARPS", 8);
+  return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
+                  : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);
 }
 
 // fp64 exceptional cases: batch-blocked DMMA tiles (k_dmma.cuh), as given or

@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 namespace sbt {
 
@@ -46,9 +47,17 @@ inline bool make_tmap_f32(CUtensorMap* map, const float* base, int64_t d0, int64
     if (dims[i] == 0 || dims[i] > (cuuint64_t(1) << 32)) return false;
   cuuint32_t box[4] = {b0, b1, b2, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
+  static const CUtensorMapL2promotion promo = [] {
+    const char* v = std::getenv("SBT_TMA_L2PROMO");  // diagnostics: 0 none, 1 64B, 2 128B, 3 256B
+    const int i = v ? std::atoi(v) : 3;
+    return i == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : i == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : i == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

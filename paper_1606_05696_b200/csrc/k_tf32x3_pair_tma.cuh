@@ -64,19 +64,26 @@ constexpr int kGroupWarps = 4;
 // is the deeper one; a smaller BK gives more, finer slots in flight.
 // BB: the converted slot also holds A_hi (the converter re-lays the dense raw
 // A box into the swizzled MN-major atom), so it is 3 operand halves wide.
-template <int BK, bool BB = false>
+// BNT: tile width (N of the MMA): 256, or 128 for N = 128 problems (each CTA
+// then holds 64 columns of B; the 2 x 128 TMEM columns also leave room for
+// double-buffered split accumulators).
+template <int BK, bool BB = false, int BNT = 256>
 struct Geo {
-  static constexpr int OP_BYTES = 128 * BK * 4;    // one operand half (A or B-half)
-  static constexpr int SLOT_BYTES = 2 * OP_BYTES;  // A half + B half
-  static constexpr int LO_SLOT_BYTES = (BB ? 3 : 2) * OP_BYTES;
+  static constexpr int A_BYTES = 128 * BK * 4;               // A half (128 rows)
+  static constexpr int B_BYTES = (BNT / 2) * BK * 4;         // B half (BNT/2 columns)
+  static constexpr int OP_BYTES = A_BYTES;
+  static constexpr int SLOT_BYTES = A_BYTES + B_BYTES;       // raw A half + raw B half
+  static constexpr int LO_SLOT_BYTES = SLOT_BYTES + (BB ? A_BYTES : 0);
+  static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
   // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles
   // (measured), ~3 K-blocks of MMA time, and a raw slot stays held until the
   // MMAs that read it retire
-  static constexpr int RAW_SLOTS = (BB ? 4 : 5) * (BK == 32 ? 1 : 2);
-  static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
+  static constexpr int RAW_SLOTS = (232448 - 1024 - 512 - LO_SLOTS * LO_SLOT_BYTES) / SLOT_BYTES;
   static constexpr int SMEM_BYTES = RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES + 1024 + 512;
-  static constexpr uint32_t TX = SLOT_BYTES;       // raw A + raw B per K-block
-  static constexpr int VEC = OP_BYTES / 16 / 128;  // float4 per converter thread per operand
+  static constexpr uint32_t TX = SLOT_BYTES;                 // raw A + raw B per K-block
+  static constexpr int NV = SLOT_BYTES / 16 / 128;           // float4 per converter thread
+  static_assert(NV % 4 == 0, "converter chunks");
+  static_assert(RAW_SLOTS <= 16, "barrier area");
 };
 
 // Debug timeline (SBT_TRACE builds only): per-event clock64 stamps of pair 0.
@@ -105,24 +112,24 @@ struct Fold {
 };
 
 // BB tiles cover 64 m (32 per CTA) x 4 batch entries; pb is then the batch group
-template <bool BB = false>
+template <bool BB = false, int BNT = BN>
 __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tiles_n,
                                         int64_t batch) {
   Tile c;
   c.m0 = (t % tiles_m) * (BB ? 64 : BM);
   t /= tiles_m;
-  c.n0 = (t % tiles_n) * BN;
+  c.n0 = (t % tiles_n) * BNT;
   t /= tiles_n;
   c.pb = t % batch;
   c.qb = t / batch;
   return c;
 }
 
-// TMA loads of one operand half (128 rows/cols of the MMA dimension x BK k).
-// K-major: one box (BK k, 128 mn).  MN-major: four boxes (32 mn, BK k), one per
-// 32-wide MN atom column, each a contiguous slab of BK 128-byte rows.
-// PREFETCH: the same boxes as L2 prefetches (no smem destination).
-template <bool KMAJ, int BK, bool PREFETCH = false>
+// TMA loads of one operand half (ROWS = 128 or 64 rows/cols of the MMA
+// dimension x BK k).  K-major: one box (BK k, ROWS mn).  MN-major: ROWS/32 boxes
+// (32 mn, BK k), one per 32-wide MN atom column, each a contiguous slab of BK
+// 128-byte rows.  PREFETCH: the same boxes as L2 prefetches (no smem).
+template <bool KMAJ, int BK, bool PREFETCH = false, int ROWS = 128>
 __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar,
                                             int64_t mn0, int64_t k0, int64_t b, int64_t b2,
                                             bool bcast, bool bcast2) {
@@ -132,14 +139,14 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst,
     else ptx::tma_load_4d(dst, tm, bar, int(k0), int(mn0), cb, cb2);
   } else {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < ROWS / 32; ++c) {
       if (PREFETCH) ptx::tma_prefetch_4d(tm, int(mn0 + 32 * c), int(k0), cb, cb2);
       else ptx::tma_load_4d(dst + c * (BK * 128), tm, bar, int(mn0 + 32 * c), int(k0), cb, cb2);
     }
   }
 }
 
-template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false>
+template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
@@ -148,7 +155,8 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   // number of batch units the tile index runs over (BB: groups of 4 entries;
   // a folded batch mode is not a tile dimension)
   const int64_t nbatch = BB ? (p.batch + 3) / 4 : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
-  using Gm = Geo<BK, BB>;
+  using Gm = Geo<BK, BB, BNT>;
+  constexpr int HNT = BNT / 2;  // B columns per CTA
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
   constexpr int LO_SLOT_BYTES = Gm::LO_SLOT_BYTES;
@@ -173,7 +181,9 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   const int64_t pair = blockIdx.x >> 1;
   const int64_t npairs = gridDim.x >> 1;
   const int nkb = int((p.k + BK - 1) / BK);
-  constexpr int NBUF = SPLIT_ACC ? 1 : 2;
+  // TMEM: NBUF buffers of (main [+ small]) BNT-column accumulators in 512 columns
+  constexpr int ACC_W = (SPLIT_ACC ? 2 : 1) * BNT;
+  constexpr int NBUF = 512 / ACC_W >= 2 ? 2 : 1;
 
   if (warp == 12) {
     if (lane == 0) {
@@ -211,11 +221,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         int am, ab, ab2, bn, bb, bb2;
       };
       auto decode = [&](int64_t tile_idx) {
-        const Tile tc = tile_of<BB>(tile_idx, tiles_m, tiles_n, nbatch);
+        const Tile tc = tile_of<BB, BNT>(tile_idx, tiles_m, tiles_n, nbatch);
         Coord c;
         if (BB) {
           c.am = int(tc.m0 + rank * 32); c.ab = int(tc.pb * 4); c.ab2 = a_bc2 ? 0 : int(tc.qb);
-          c.bn = int(tc.n0 + rank * HN); c.bb = b_bc ? 0 : int(tc.pb); c.bb2 = b_bc2 ? 0 : int(tc.qb);
+          c.bn = int(tc.n0 + rank * HNT); c.bb = b_bc ? 0 : int(tc.pb); c.bb2 = b_bc2 ? 0 : int(tc.qb);
           return c;
         }
         // (un)fold: CTA row / column block -> (inner index, folded batch index)
@@ -225,7 +235,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           am -= x * f.m_in;
           if (f.fm == 1) ab = x; else ab2 = x;
         }
-        int64_t bn = tc.n0 + rank * HN, bb = tc.pb, bb2 = tc.qb;
+        int64_t bn = tc.n0 + rank * HNT, bb = tc.pb, bb2 = tc.qb;
         if (f.fn) {
           const int64_t y = bn / f.n_in;
           bn -= y * f.n_in;
@@ -248,7 +258,8 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         } else {
           tma_operand<A_K, BK, PF>(&tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
         }
-        tma_operand<B_K, BK, PF>(&tmB, st + OP_BYTES, bar, c.bn, k0, c.bb, c.bb2, false, false);
+        tma_operand<B_K, BK, PF, HNT>(&tmB, st + Gm::A_BYTES, bar, c.bn, k0, c.bb, c.bb2, false,
+                                      false);
       };
       // L2 prefetch distance (K-blocks ahead of the smem ring)
       const int pfd = p_prefetch & 0xff;
@@ -300,19 +311,19 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       ptx::mbar_wait(&raw_full[s], uint32_t(g / RAW_SLOTS) & 1u);
       if (ct == 0) TRACE(1, int(g));
       const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
-      constexpr int NV = 2 * Gm::VEC;  // float4 chunks per thread (A and B halves)
+      constexpr int NV = Gm::NV;  // float4 chunks per thread (A and B halves)
 #pragma unroll
-      for (int h = 0; h < ((p_prefetch >> 9) & 1 ? 0 : NV / 8); ++h) {
-        float4 v[8];
+      for (int h = 0; h < ((p_prefetch >> 9) & 1 ? 0 : NV / 4); ++h) {
+        float4 v[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 8 + i) * 128) * 16);
+        for (int i = 0; i < 4; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 4 + i) * 128) * 16);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uint32_t off = (ct + (h * 8 + i) * 128) * 16;
-          if (BB && (h * 8 + i) * 128 < OP_BYTES / 16) {  // chunk lies in the A half
+        for (int i = 0; i < 4; ++i) {
+          uint32_t off = (ct + (h * 4 + i) * 128) * 16;
+          if (BB && (h * 4 + i) * 128 < Gm::A_BYTES / 16) {  // chunk lies in the A half
             // dense [k][m8][b4] A chunk -> 32 B-atom swizzle (k row % 4 XOR granule)
             off ^= ((off >> 7) & 3u) << 5;
-            ptx::sts_v4(lo_base + 2 * OP_BYTES + off, __float_as_uint(v[i].x),
+            ptx::sts_v4(lo_base + Gm::SLOT_BYTES + off, __float_as_uint(v[i].x),
                         __float_as_uint(v[i].y), __float_as_uint(v[i].z), __float_as_uint(v[i].w));
           }
           ptx::sts_v4(lo_base + off, __float_as_uint(ptx::tf32_residual(v[i].x)),
@@ -357,11 +368,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       float* __restrict__ crow =
           p.c + (row_ok ? bidx * p.cps + row * p.crs + qidx * p.cps2 : 0);
       const int64_t ncols = BB ? p.n : f.ntot;
-      const bool full_tile = (tc.n0 + BN <= ncols) && p.beta == 0.f;
+      const bool full_tile = (tc.n0 + BNT <= ncols) && p.beta == 0.f;
       const bool vec = (p.ccs == 1) && full_tile;
-      const uint32_t acc_col = SPLIT_ACC ? 0u : b * BN;
+      const uint32_t acc_col = b * ACC_W;
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 16) {
+      for (int cc = 0; cc < BNT; cc += 16) {
         uint32_t v[16];
         float o[16];
 #ifdef SBT_TRACE
@@ -370,7 +381,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         ptx::tmem_ld16(tmem + lane_addr + acc_col + cc, v);
         if (SPLIT_ACC) {
           uint32_t w[16];
-          ptx::tmem_ld16(tmem + lane_addr + BN + cc, w);
+          ptx::tmem_ld16(tmem + lane_addr + acc_col + BNT + cc, w);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]) + __uint_as_float(w[j]);
@@ -427,7 +438,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     }
   } else if (warp == 13 && rank == 0 && lane == 0) {
     // -------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, !A_K, !B_K);
+    constexpr uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);
     // K-major: rows of BK*4 bytes (SW128 for BK=32, SW64 for BK=16), 8-row
     // groups at SBO = 8*BK*4, K=8 step = 32 B inside the row.
     // MN-major: 32-wide MN slabs of BK k-rows: LBO = slab stride (BK*128 B),
@@ -444,19 +455,19 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_empty[b], ph ^ 1u);
       ptx::tc_fence_after();
-      const uint32_t d_main = tmem + (SPLIT_ACC ? 0u : b * BN);
-      const uint32_t d_small = SPLIT_ACC ? tmem + BN : d_main;
+      const uint32_t d_main = tmem + b * ACC_W;
+      const uint32_t d_small = SPLIT_ACC ? d_main + BNT : d_main;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t s = it % RAW_SLOTS;
         const uint32_t ls = it % LO_SLOTS;
         ptx::mbar_wait(&full[s], (it / RAW_SLOTS) & 1u);
         TRACE(3, int(it));
         ptx::tc_fence_after();
-        const uint32_t b_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES) + OP_BYTES;
+        const uint32_t b_raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES) + Gm::A_BYTES;
         const uint32_t a_lo = ptx::smem_addr(lo_ring + ls * LO_SLOT_BYTES);
-        const uint32_t b_lo = a_lo + OP_BYTES;
+        const uint32_t b_lo = a_lo + Gm::A_BYTES;
         // BB: A_hi is the converter's swizzled copy, not the dense raw box
-        const uint32_t a_raw = BB ? a_lo + 2 * OP_BYTES : b_raw - OP_BYTES;
+        const uint32_t a_raw = BB ? a_lo + Gm::SLOT_BYTES : b_raw - Gm::A_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);

@@ -135,12 +135,13 @@ static tf32tma::Fold make_fold(const GemmParams<float>& p) {
   return f;
 }
 
-template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false>
+template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false, int BNT = 256>
 static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
                              tf32tma::Fold f = tf32tma::Fold{0, 0, 0, 0, 0, 0}) {
   if (f.mtot == 0) f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0};
-  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB>;
-  constexpr int smem = tf32tma::Geo<KB, BB>::SMEM_BYTES;
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB, BNT>;
+  constexpr int smem = tf32tma::Geo<KB, BB, BNT>::SMEM_BYTES;
+  constexpr uint32_t HNT = BNT / 2;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -158,13 +159,13 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
            : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, KB,
                            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const bool ok_b =
-      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB, 128,
+      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB, HNT,
                           kswz)
           : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
   const int64_t tiles_m = ceil_div(f.mtot, BB ? 64 : tf32tma::BM);
-  const int64_t tiles_n = ceil_div(f.ntot, tf32tma::BN);
+  const int64_t tiles_n = ceil_div(f.ntot, BNT);
   const int64_t nb = BB ? ceil_div(p.batch, 4) : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
   const int64_t nb2 = (f.fm == 2 || f.fn == 2) ? 1 : p.batch2;
   const int64_t total = tiles_m * tiles_n * nb * nb2;
@@ -175,8 +176,12 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
       p, ta, tb, tiles_m, tiles_n, total, f, prefetch);
   note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
-                 : (f.fm || f.fn) ? (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold")
-                 : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma"));
+                 : (f.fm || f.fn)
+                     ? (BNT == 128 ? (SPLIT ? "tc_tf32x3_pair_fold_n128_splitacc"
+                                            : "tc_tf32x3_pair_fold_n128")
+                                   : (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold"))
+                     : (BNT == 128 ? (SPLIT ? "tc_tf32x3_pair_n128_splitacc" : "tc_tf32x3_pair_n128")
+                                   : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma")));
   return 1;
 }
 
@@ -195,30 +200,26 @@ static int launch_tf32_bb(const GemmParams<float>& p0, cudaStream_t stream) {
     if (p.m < 64 || p.n < 192) continue;
     const int bm = b_major(p);
     if (!bm) continue;
-    if (bm == 1)
-      return kb == 16 ? launch_tf32tma_kb<false, true, SPLIT, 16, true>(p, stream)
-                      : launch_tf32tma_kb<false, true, SPLIT, 32, true>(p, stream);
-    return kb == 16 ? launch_tf32tma_kb<false, false, SPLIT, 16, true>(p, stream)
-                    : launch_tf32tma_kb<false, false, SPLIT, 32, true>(p, stream);
+    (void)kb;  // BK = 32 only (the BK = 16 variant measured slower)
+    if (bm == 1) return launch_tf32tma_kb<false, true, SPLIT, 32, true>(p, stream);
+    return launch_tf32tma_kb<false, false, SPLIT, 32, true>(p, stream);
   }
   return 0;
 }
 
-template <bool AK, bool BK_, bool SPLIT>
+template <bool AK, bool BK_, bool SPLIT, int BNT>
 static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream,
                               const tf32tma::Fold& f) {
-  static const int kb = env_int("SBT_TC_BK", 32);
-  return kb == 16 ? launch_tf32tma_kb<AK, BK_, SPLIT, 16>(p, stream, f)
-                  : launch_tf32tma_kb<AK, BK_, SPLIT, 32>(p, stream, f);
+  return launch_tf32tma_kb<AK, BK_, SPLIT, 32, false, BNT>(p, stream, f);
 }
 
-template <bool SPLIT>
+template <bool SPLIT, int BNT>
 static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
                           const tf32tma::Fold& f) {
-  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT>(p, s, f);
-  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT>(p, s, f);
-  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT>(p, s, f);
-  return launch_tf32tma_cfg<false, false, SPLIT>(p, s, f);
+  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f);
+  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT, BNT>(p, s, f);
+  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
+  return launch_tf32tma_cfg<false, false, SPLIT, BNT>(p, s, f);
 }
 
 template <int BN>
@@ -335,22 +336,42 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
     const int rc = split ? launch_tf32_bb<true>(p0, stream) : launch_tf32_bb<false>(p0, stream);
     if (rc != 0) return rc;
   }
+  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair,
+  // 6 = auto without batch folding
+  if (variant == 0 || variant == 4 || variant == 6) {
+    // CTA-pair kernel: among the two orientations (C = AB, C^T = B^T A^T) take
+    // the one whose (folded) M reaches a full 256-row tile, larger M first;
+    // tile width 256, or 128 when N' < 192
+    GemmParams<float> best{};
+    tf32tma::Fold bf{};
+    int ba = 0, bb = 0;
+    bool found = false;
+    for (int o = 0; o < 2; ++o) {
+      const GemmParams<float> q = o ? transposed(p0) : p0;
+      const int qa = a_major(q), qb = b_major(q);
+      if (!qa || !qb) continue;
+      const tf32tma::Fold f = variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0} : make_fold(q);
+      const bool ok = variant == 4 || (f.mtot >= 256 && f.ntot >= 96);
+      if (ok && (!found || f.mtot > bf.mtot || (f.mtot == bf.mtot && f.ntot > bf.ntot))) {
+        best = q; bf = f; ba = qa; bb = qb; found = true;
+      }
+    }
+    if (found) {
+      static const int split_env = env_int("SBT_TC_SPLITACC", -1);
+      const bool split = split_env < 0 ? (best.k > 512) : (split_env != 0);
+      const bool n128 = bf.ntot < 192;
+      const int rc = split ? (n128 ? launch_tf32tma<true, 128>(best, ba, bb, stream, bf)
+                                   : launch_tf32tma<true, 256>(best, ba, bb, stream, bf))
+                           : (n128 ? launch_tf32tma<false, 128>(best, ba, bb, stream, bf)
+                                   : launch_tf32tma<false, 256>(best, ba, bb, stream, bf));
+      if (rc != 0) return rc;
+    }
+  }
   GemmParams<float> p;
   int am = 0, bm = 0;
   if (!orient(p0, &p, &am, &bm)) return 0;
   if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
-  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair,
-  // 6 = auto without batch folding
-  const tf32tma::Fold fold = variant == 6 ? tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0} : make_fold(p);
-  if (((variant == 0 || variant == 6) && fold.ntot >= 192 && fold.mtot >= 256) ||
-      variant == 4) {
-    static const int split_env = env_int("SBT_TC_SPLITACC", -1);
-    const bool split = split_env < 0 ? (p.k > 512) : (split_env != 0);
-    const int rc = split ? launch_tf32tma<true>(p, am, bm, stream, fold)
-                         : launch_tf32tma<false>(p, am, bm, stream, fold);
-    if (rc != 0) return rc;
-  }
   int bn = env_int("SBT_TC_BN", 0);
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256)
     bn = p.n > 128 ? 256 : (p.n > 64 ? 128 : (p.n > 32 ? 64 : 32));

@@ -75,11 +75,15 @@ struct Geo {
   static constexpr int SLOT_BYTES = A_BYTES + B_BYTES;       // raw A half + raw B half
   static constexpr int LO_SLOT_BYTES = SLOT_BYTES + (BB ? A_BYTES : 0);
   static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
+  // epilogue staging for the TMA-store epilogue: 2 x (128 rows x 32 columns)
+  static constexpr int EPI_BYTES = BB ? 0 : 2 * 128 * 32 * 4;
   // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles
   // (measured), ~3 K-blocks of MMA time, and a raw slot stays held until the
   // MMAs that read it retire
-  static constexpr int RAW_SLOTS = (232448 - 1024 - 512 - LO_SLOTS * LO_SLOT_BYTES) / SLOT_BYTES;
-  static constexpr int SMEM_BYTES = RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES + 1024 + 512;
+  static constexpr int RAW_SLOTS =
+      (232448 - 1024 - 512 - LO_SLOTS * LO_SLOT_BYTES - EPI_BYTES) / SLOT_BYTES;
+  static constexpr int SMEM_BYTES =
+      RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES + EPI_BYTES + 1024 + 512;
   static constexpr uint32_t TX = SLOT_BYTES;                 // raw A + raw B per K-block
   static constexpr int NV = SLOT_BYTES / 16 / 128;           // float4 per converter thread
   static_assert(NV % 4 == 0, "converter chunks");
@@ -109,6 +113,9 @@ struct Fold {
   int64_t m_in, n_in;  // inner extents (p.m, p.n)
   int64_t mtot, ntot;  // folded extents M', N'
   int fm, fn;          // 0 = none, 1 = folds `batch`, 2 = folds `batch2`
+  // epilogue: 0 = direct st.global; TMA store through smem staging with the C
+  // tensor map over (1) rows contiguous (crs = 1) or (2) columns contiguous
+  int cmode;
 };
 
 // BB tiles cover 64 m (32 per CTA) x 4 batch entries; pb is then the batch group
@@ -149,7 +156,8 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst,
 template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
-                       const __grid_constant__ CUtensorMap tmB, int64_t tiles_m,
+                       const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmC, int64_t tiles_m,
                        int64_t tiles_n, int64_t total, Fold f, int p_prefetch) {
   static_assert(!(BB && A_K), "batch-blocked A is MN-major");
   // number of batch units the tile index runs over (BB: groups of 4 entries;
@@ -165,8 +173,8 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw_ring = smem;
   uint8_t* lo_ring = smem + RAW_SLOTS * SLOT_BYTES;
-  uint64_t* raw_full =
-      reinterpret_cast<uint64_t*>(smem + RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES);
+  uint8_t* epi_stage = smem + RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES;  // 1 KB aligned
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(epi_stage + Gm::EPI_BYTES);
   uint64_t* raw_empty = raw_full + RAW_SLOTS;
   uint64_t* full = raw_empty + RAW_SLOTS;         // converted (leader's copy is the one used)
   uint64_t* lo_empty = full + RAW_SLOTS;
@@ -200,6 +208,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       ptx::fence_mbarrier_init();
       ptx::prefetch_tmap(&tmA);
       ptx::prefetch_tmap(&tmB);
+      if (!BB && f.cmode) ptx::prefetch_tmap(&tmC);
     }
     __syncwarp();
     ptx::tmem_alloc2(tmem_slot, 512);
@@ -344,9 +353,95 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     // -------------------------------------------------------- epilogue
     const uint32_t lane_addr = uint32_t(warp * 32) << 16;
     const uint32_t empty_leader[2] = {ptx::mapa(&acc_empty[0], 0), ptx::mapa(&acc_empty[1], 0)};
+    if (!BB && f.cmode) {
+      // TMA-store epilogue: per 32-column chunk, TMEM -> registers (alpha) ->
+      // smem staging (double-buffered) -> one TMA store of a 128 x 32 box.
+      // The TMA engine writes full lines and clips the M / N tails.
+      const int r = warp * 32 + lane;
+      const bool leader = (r == 0);
+      uint32_t nchunk = 0, tcount = 0;
+      for (int64_t t = pair; t < total; t += npairs, ++tcount) {
+        const Tile tc = tile_of<BB, BNT>(t, tiles_m, tiles_n, nbatch);
+        const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
+        const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
+        ptx::mbar_wait(&acc_full[b], ph);
+        ptx::tc_fence_after();
+        // CTA row block -> (inner row, folded batch index)
+        int64_t row0 = tc.m0 + rank * HM, rb = tc.pb, rb2 = tc.qb;
+        if (f.fm) {
+          const int64_t x = row0 / f.m_in;
+          row0 -= x * f.m_in;
+          if (f.fm == 1) rb = x; else rb2 = x;
+        }
+        const uint32_t acc_col = b * ACC_W;
+#pragma unroll 1
+        for (int cc = 0; cc < BNT; cc += 32, ++nchunk) {
+          uint32_t v[32];
+          ptx::tmem_ld16(tmem + lane_addr + acc_col + cc, *reinterpret_cast<uint32_t(*)[16]>(v));
+          ptx::tmem_ld16(tmem + lane_addr + acc_col + cc + 16,
+                         *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+          float o[32];
+          if (SPLIT_ACC) {
+            uint32_t w[32];
+            ptx::tmem_ld16(tmem + lane_addr + acc_col + BNT + cc,
+                           *reinterpret_cast<uint32_t(*)[16]>(w));
+            ptx::tmem_ld16(tmem + lane_addr + acc_col + BNT + cc + 16,
+                           *reinterpret_cast<uint32_t(*)[16]>(w + 16));
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              o[j] = p.alpha * (__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          } else {
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = p.alpha * __uint_as_float(v[j]);
+          }
+          if (cc + 32 == BNT) {  // accumulator buffer drained: hand it back to the MMA
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (rank == 0) ptx::mbar_arrive(&acc_empty[b]);
+              else ptx::mbar_arrive_remote(empty_leader[b]);
+            }
+          }
+          const uint32_t buf = nchunk & 1u;
+          const uint32_t stg = ptx::smem_addr(epi_stage + buf * (128 * 32 * 4));
+          if (leader) ptx::bulk_wait_group_read<1>();  // the store that used `buf` read it
+          ptx::named_bar_sync(1, 128);
+          if (f.cmode == 1) {  // [32 cols][128 rows]: a warp writes 128 B per column
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ptx::sts_f32(stg + j * 512 + r * 4, o[j]);
+          } else {  // [128 rows][32 cols], 128 B swizzle (16 B chunk q at q ^ (row & 7))
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              ptx::sts_v4(stg + r * 128 + ((q ^ (r & 7)) << 4), __float_as_uint(o[4 * q]),
+                          __float_as_uint(o[4 * q + 1]), __float_as_uint(o[4 * q + 2]),
+                          __float_as_uint(o[4 * q + 3]));
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(1, 128);
+          if (leader) {
+            int64_t col0 = tc.n0 + cc, cb = rb, cb2 = rb2;
+            if (f.fn) {
+              const int64_t y = col0 / f.n_in;
+              col0 -= y * f.n_in;
+              if (f.fn == 1) cb = y; else cb2 = y;
+            }
+            if (f.cmode == 1)
+              ptx::tma_store_4d(&tmC, epi_stage + buf * (128 * 32 * 4), int(row0), int(col0),
+                                int(cb), int(cb2));
+            else
+              ptx::tma_store_4d(&tmC, epi_stage + buf * (128 * 32 * 4), int(col0), int(row0),
+                                int(cb), int(cb2));
+            ptx::bulk_commit_group();
+          }
+        }
+      }
+      if (leader) ptx::bulk_wait_group<0>();
+    } else {
     uint32_t tcount = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-      const Tile tc = tile_of<BB>(t, tiles_m, tiles_n, nbatch);
+      const Tile tc = tile_of<BB, BNT>(t, tiles_m, tiles_n, nbatch);
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_full[b], ph);
@@ -436,6 +531,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         else ptx::mbar_arrive_remote(empty_leader[b]);
       }
     }
+    }  // direct-store epilogue
   } else if (warp == 13 && rank == 0 && lane == 0) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);

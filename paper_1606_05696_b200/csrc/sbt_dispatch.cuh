@@ -10,6 +10,7 @@
 //   generic SIMT kernel for everything else (odd extents / strides).
 #pragma once
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "sbt_common.cuh"
@@ -112,7 +113,7 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
 // and C) when the extent is a multiple of the CTA block but not of the 256-wide
 // pair tile (see k_tf32x3_pair_tma.cuh, struct Fold).
 static tf32tma::Fold make_fold(const GemmParams<float>& p) {
-  tf32tma::Fold f{p.m, p.n, p.m, p.n, 0, 0};
+  tf32tma::Fold f{p.m, p.n, p.m, p.n, 0, 0, 0};
   auto cnt = [&](int w) { return w == 1 ? p.batch : p.batch2; };
   auto as = [&](int w) { return w == 1 ? p.aps : p.aps2; };
   auto bs = [&](int w) { return w == 1 ? p.bps : p.bps2; };
@@ -137,8 +138,8 @@ static tf32tma::Fold make_fold(const GemmParams<float>& p) {
 
 template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false, int BNT = 256>
 static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
-                             tf32tma::Fold f = tf32tma::Fold{0, 0, 0, 0, 0, 0}) {
-  if (f.mtot == 0) f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0};
+                             tf32tma::Fold f = tf32tma::Fold{0, 0, 0, 0, 0, 0, 0}) {
+  if (f.mtot == 0) f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0, 0};
   auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB, BNT>;
   constexpr int smem = tf32tma::Geo<KB, BB, BNT>::SMEM_BYTES;
   constexpr uint32_t HNT = BNT / 2;
@@ -164,6 +165,22 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
           : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
+  // TMA-store epilogue when C is expressible as a tensor map (beta == 0: C not read)
+  CUtensorMap tcm;
+  std::memset(&tcm, 0, sizeof(tcm));
+  f.cmode = 0;
+  static const int tma_epi = env_int("SBT_TC_TMA_EPI", 1);
+  if (!BB && tma_epi && p.beta == 0.f && aligned16(p.c) && vmult<float>(p.cps) &&
+      vmult<float>(p.cps2)) {
+    if (p.crs == 1 && vmult<float>(p.ccs) &&
+        make_tmap_f32(&tcm, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 128, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+      f.cmode = 1;
+    else if (p.ccs == 1 && vmult<float>(p.crs) &&
+             make_tmap_f32(&tcm, p.c, p.n, p.m, p.crs, p.batch, p.cps, p.batch2, p.cps2, 32, 128,
+                           CU_TENSOR_MAP_SWIZZLE_128B))
+      f.cmode = 2;
+  }
   const int64_t tiles_m = ceil_div(f.mtot, BB ? 64 : tf32tma::BM);
   const int64_t tiles_n = ceil_div(f.ntot, BNT);
   const int64_t nb = BB ? ceil_div(p.batch, 4) : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
@@ -174,7 +191,7 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
   // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
   static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8);
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
-      p, ta, tb, tiles_m, tiles_n, total, f, prefetch);
+      p, ta, tb, tcm, tiles_m, tiles_n, total, f, prefetch);
   note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
                  : (f.fm || f.fn)
                      ? (BNT == 128 ? (SPLIT ? "tc_tf32x3_pair_fold_n128_splitacc"
@@ -350,7 +367,7 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
       const GemmParams<float> q = o ? transposed(p0) : p0;
       const int qa = a_major(q), qb = b_major(q);
       if (!qa || !qb) continue;
-      const tf32tma::Fold f = variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0} : make_fold(q);
+      const tf32tma::Fold f = variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q);
       const bool ok = variant == 4 || (f.mtot >= 256 && f.ntot >= 96);
       if (ok && (!found || f.mtot > bf.mtot || (f.mtot == bf.mtot && f.ntot > bf.ntot))) {
         best = q; bf = f; ba = qa; bb = qb; found = true;

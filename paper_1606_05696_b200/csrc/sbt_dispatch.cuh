@@ -510,17 +510,31 @@ static int launch_chunked(const GemmParams<T>& p, cudaStream_t stream);
 
 template <typename T>
 static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
-  if (p.batch != 1 || p.batch2 != 1 || p.k < 16384) return 0;
+  // fp64 (DMMA, 128x128 tiles): worth splitting from K = 1024 (HOOI Grams:
+  // 512 x 512 with K = 1024 would otherwise occupy 16 of 148 SMs); fp32 tiles
+  // are larger and faster, so only very long reductions split
+  const int64_t min_k = sizeof(T) == 8 ? 1024 : 16384, min_chunk = sizeof(T) == 8 ? 256 : 4096;
+  if (p.batch != 1 || p.batch2 != 1 || p.k < min_k) return 0;
   const int64_t tiles = ceil_div(p.m, 128) * ceil_div(p.n, 128);
   if (tiles >= kNumSMs / 2) return 0;
   int64_t S = (2 * kNumSMs) / tiles;
-  const int64_t max_s = p.k / 4096;
+  const int64_t max_s = p.k / min_chunk;
   if (S > max_s) S = max_s;
   if (S < 2) return 0;
   // chunk length: multiple of 32 so every chunk keeps the operands' alignment
   const int64_t kc = ((ceil_div(p.k, S) + 31) / 32) * 32;
   S = ceil_div(p.k, kc);
   T* w = nullptr;
+  static bool pool_kept = [] {  // keep freed workspaces in the stream-ordered pool
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return true;
+  }();
+  (void)pool_kept;
   if (cudaMallocAsync(reinterpret_cast<void**>(&w), size_t(S) * p.m * p.n * sizeof(T), stream) !=
       cudaSuccess)
     return -3;

@@ -510,10 +510,12 @@ static int launch_chunked(const GemmParams<T>& p, cudaStream_t stream);
 
 template <typename T>
 static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
-  // fp64 (DMMA, 128x128 tiles): worth splitting from K = 1024 (HOOI Grams:
-  // 512 x 512 with K = 1024 would otherwise occupy 16 of 148 SMs); fp32 tiles
-  // are larger and faster, so only very long reductions split
-  const int64_t min_k = sizeof(T) == 8 ? 1024 : 16384, min_chunk = sizeof(T) == 8 ? 256 : 4096;
+  // fp64 (DMMA, 128x128 tiles, 4096 cycles per 16-deep K step): split as soon
+  // as few tiles leave SMs idle -- the HOOI Grams (512 x 512, K = 1024) and the
+  // Rayleigh-Ritz products (512 x 48 and 48 x 48, K = 512) would otherwise run
+  // on 16 / 4 / 1 CTAs; fp32 tiles are larger and faster, so only very long
+  // reductions split
+  const int64_t min_k = sizeof(T) == 8 ? 256 : 16384, min_chunk = sizeof(T) == 8 ? 64 : 4096;
   if (p.batch != 1 || p.batch2 != 1 || p.k < min_k) return 0;
   const int64_t tiles = ceil_div(p.m, 128) * ceil_div(p.n, 128);
   if (tiles >= kNumSMs / 2) return 0;
@@ -523,6 +525,7 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
   if (S < 2) return 0;
   // chunk length: multiple of 32 so every chunk keeps the operands' alignment
   const int64_t kc = ((ceil_div(p.k, S) + 31) / 32) * 32;
+  if (kc >= p.k) return 0;
   S = ceil_div(p.k, kc);
   T* w = nullptr;
   static bool pool_kept = [] {  // keep freed workspaces in the stream-ordered pool
@@ -541,11 +544,12 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
   GemmParams<T> q = p;
   q.alpha = T(1); q.beta = T(0);
   q.c = w; q.crs = 1; q.ccs = p.m; q.cps = p.m * p.n;
-  q.k = kc; q.batch = S - 1;             // full chunks
+  const bool even = p.k == S * kc;
+  q.k = kc; q.batch = even ? S : S - 1;   // full chunks
   q.aps = kc * p.acs; q.bps = kc * p.brs;
   int rc = 0;
   if (q.batch > 0) rc = launch_chunked<T>(q, stream);
-  if (rc == 0) {                          // ragged last chunk
+  if (rc == 0 && !even) {                 // ragged last chunk
     GemmParams<T> t = q;
     t.batch = 1; t.k = p.k - (S - 1) * kc;
     t.a = p.a + (S - 1) * kc * p.acs; t.b = p.b + (S - 1) * kc * p.brs;

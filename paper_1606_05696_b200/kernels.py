@@ -181,8 +181,13 @@ def core_call(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta, 
         raise ValueError(f"unsupported dtype {da}")
     if not (a.device == b.device == c.device):
         raise ValueError("A, B and C must be on the same device")
-    stream = torch.cuda.current_stream(c.device).cuda_stream
-    with torch.cuda.device(c.device):
+    dev = c.device.index
+    if dev != torch.cuda.current_device():    # launch on C's device
+        with torch.cuda.device(dev):
+            return core_call(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta,
+                             c, oc, crs, ccs, cpt, batch, apt2, bpt2, cpt2, batch2, extended)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if True:
         if batch2 != 1:
             fn = lib.sbt_batched2_core_f64 if f64 else lib.sbt_batched2_core_f32
             rc = fn(m, n, k, alpha, a.data_ptr(), oa, ars, acs, apt, apt2, b.data_ptr(), ob,

@@ -545,6 +545,36 @@ def run_config(args):
                            "init_plus_one_iter_ms": round(t_init * 1e3, 1),
                            "contraction_gflop_per_iter": round(fl / 1e9, 2),
                            "fit_history": [round(f, 8) for f in model.fit_history]}}
+    elif args.config == "conventional":
+        # the paper's comparison (Fig. 1/4) on the device: every case
+        # as planned (transpose-free, one launch) vs conventional
+        # permute-then-GEMM (reference planner.py:411-465, policy "opt")
+        import paper_1606_05696_b200 as sbt
+        n = args.n
+        cases = case_shapes(n)
+        work = build_sets(cases, n, dtype, "cuda", 2, seed=7)
+        per = {}
+        tot_sb = tot_conv = 0.0
+        for cid, plan, a, b, c in work:
+            conv = sbt.plan_conventional(plan.spec, a.layout, b.layout, c.layout, policy="opt")
+            ms_sb = _time_steps(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), args.steps,
+                                args.warmup)
+            ms_cv = _time_steps(lambda: execute_plan(conv, a, b, 1.0, 0.0, c), args.steps,
+                                args.warmup)
+            tot_sb += ms_sb
+            tot_conv += ms_cv
+            per[cid] = {"sbgemm_ms": round(ms_sb, 4), "conventional_ms": round(ms_cv, 4),
+                        "transpositions": conv.predicted_transpositions,
+                        "speedup": round(ms_cv / ms_sb, 2)}
+        fl = 2.0 * n ** 4 * len(work)
+        line = {"metric": "transpose-free SBGEMM vs conventional permute+GEMM (36 cases)",
+                "value": round(tot_conv / tot_sb, 3), "unit": "x (conventional time / "
+                "transpose-free time)",
+                "config": {"workload": f"36-case sweep n={n} {args.dtype}, device, "
+                                       "conventional policy opt",
+                           "sbgemm_gflops": round(fl / (tot_sb * 1e-3) / 1e9, 1),
+                           "conventional_gflops": round(fl / (tot_conv * 1e-3) / 1e9, 1)},
+                "per_case": per}
     else:
         raise SystemExit(f"unknown config {args.config}")
     line.update({"n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -636,7 +666,8 @@ def main():
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--sustained-probe", action="store_true",
                     help="also measure the power-capped (sustained) TF32 peak (~3 s)")
-    ap.add_argument("--config", choices=("sweep", "small", "order4", "hooi"), default="sweep")
+    ap.add_argument("--config", choices=("sweep", "small", "order4", "hooi", "conventional"),
+                    default="sweep")
     ap.add_argument("--batch", type=int, default=1000000)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -59,6 +59,15 @@ int sbt_probe_tf32_peak(double* tflops);
 /* The same probe run back to back for `seconds` (clocks under the power cap). */
 int sbt_probe_tf32_sustained(double seconds, double* tflops);
 
+/* ---- reference: layout.py:202-215 permute_copy (the conventional strategy's
+        explicit transposition, planner.py:620-713; NOT used by planned
+        contractions).  dst is packed column-major; its mode i has extent
+        dims[i] and is read from src with element stride src_strides[i]. */
+int sbt_permute_f64(int order, const int64_t* dims, const double* src,
+                    const int64_t* src_strides, double* dst, void* stream);
+int sbt_permute_f32(int order, const int64_t* dims, const float* src,
+                    const int64_t* src_strides, float* dst, void* stream);
+
 /* ---- reference: _loops_numba.py:12-25 gemm_core (called by kernels.gemm, kernels.py:107) */
 int sbt_gemm_core_f64(int64_t m, int64_t n, int64_t k, double alpha,
                       const double* a, int64_t oa, int64_t ars, int64_t acs,

@@ -46,6 +46,10 @@ SIGNATURES = {
     "sbt_probe_fp64_peak": ([c_int, ctypes.POINTER(c_double)], c_int),
     "sbt_probe_tf32_peak": ([ctypes.POINTER(c_double)], c_int),
     "sbt_probe_tf32_sustained": ([c_double, ctypes.POINTER(c_double)], c_int),
+    "sbt_permute_f64": ([c_int, ctypes.POINTER(c_int64), _P, ctypes.POINTER(c_int64), _P, _P],
+                        c_int),
+    "sbt_permute_f32": ([c_int, ctypes.POINTER(c_int64), _P, ctypes.POINTER(c_int64), _P, _P],
+                        c_int),
     "sbt_gemm_core_f64": (_core_sig(c_double), c_int),
     "sbt_gemm_core_f32": (_core_sig(c_float), c_int),
     "sbt_batched_core_f64": (_batched_sig(c_double), c_int),

@@ -20,6 +20,7 @@
 #include "k_generic.cuh"
 #include "sbt_dispatch.cuh"
 #include "k_probe.cuh"
+#include "k_permute.cuh"
 
 namespace sbt {
 
@@ -154,6 +155,43 @@ static int run_host(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_
 
 using namespace sbt;
 
+namespace sbt {
+// Explicit permutation copy (conventional strategy only; see k_permute.cuh).
+template <typename T>
+static int run_permute(int order, const int64_t* dims, const T* src, const int64_t* sstr, T* dst,
+                       cudaStream_t stream) {
+  if (order < 1 || order > perm::kMaxOrder || !dims || !sstr || !src || !dst)
+    return fail(SBT_EINVAL, "permute: bad arguments");
+  perm::PermParams q{};
+  q.order = order;
+  q.inner = 0;
+  int64_t total = 1, d = 1;
+  for (int i = 0; i < order; ++i) {
+    if (dims[i] < 1 || sstr[i] < 0) return fail(SBT_EINVAL, "permute: bad extent or stride");
+    q.dims[i] = dims[i];
+    q.sstr[i] = sstr[i];
+    q.dstr[i] = d;
+    d *= dims[i];
+    total *= dims[i];
+  }
+  if (sstr[0] != 1)
+    for (int i = 1; i < order; ++i)
+      if (sstr[i] == 1 && dims[i] > 1) { q.inner = i; break; }
+  q.outer = total / q.dims[0] / (q.inner ? q.dims[q.inner] : 1);
+  int64_t work = q.inner ? ceil_div(q.dims[0], 32) * ceil_div(q.dims[q.inner], 32) * q.outer : q.outer;
+  const int64_t grid = work < int64_t(kNumSMs) * 16 ? work : int64_t(kNumSMs) * 16;
+  if (q.inner) {
+    perm::permute_tile_kernel<T><<<unsigned(grid), 256, 0, stream>>>(src, dst, q);
+    note_launch("permute_tile");
+  } else {
+    perm::permute_rows_kernel<T><<<unsigned(grid), 256, 0, stream>>>(src, dst, q);
+    note_launch("permute_rows");
+  }
+  return check_cuda(cudaGetLastError(), "permute launch");
+}
+
+}  // namespace sbt
+
 extern "C" {
 
 int sbt_version(void) { return 100; }
@@ -260,6 +298,15 @@ int sbt_probe_tf32_sustained(double seconds, double* tflops) {
   cudaEventDestroy(e1);
   note_launch("probe_tf32_umma");
   return check_cuda(cudaGetLastError(), "probe");
+}
+
+int sbt_permute_f64(int order, const int64_t* dims, const double* src, const int64_t* src_strides,
+                    double* dst, void* stream) {
+  return sbt::run_permute<double>(order, dims, src, src_strides, dst, (cudaStream_t)stream);
+}
+int sbt_permute_f32(int order, const int64_t* dims, const float* src, const int64_t* src_strides,
+                    float* dst, void* stream) {
+  return sbt::run_permute<float>(order, dims, src, src_strides, dst, (cudaStream_t)stream);
 }
 
 #define SBT_DEFINE(T, SUF)                                                                     \

@@ -28,8 +28,8 @@ from dataclasses import dataclass, field
 from math import factorial, prod
 
 from .kernels import KernelArgs, Op, core_call
-from .layout import DenseTensor, Layout
-from .notation import ContractionSpec, classify_indices
+from .layout import DenseTensor, Layout, permute_copy, permute_into
+from .notation import ContractionSpec, classify_indices, kernel_family
 
 
 class PlanError(ValueError):
@@ -83,6 +83,26 @@ class BatchedStep:
     batch_label: str
     extent: int
     extended: bool = False
+
+
+@dataclass(frozen=True)
+class PermuteStep:
+    tensor: str
+    perm: tuple
+
+
+@dataclass(frozen=True)
+class ConventionalInfo:
+    free_a: tuple
+    free_b: tuple
+    contracted: tuple
+    op_a: Op
+    op_b: Op
+    permute_a: object           # tuple | None
+    permute_b: object
+    c_matches: bool             # C's label order is already free_a + free_b
+    family: str
+    policy: str
 
 
 @dataclass
@@ -376,6 +396,112 @@ def lower_plan(plan: EvaluationPlan) -> Launch:
     return plan._launch
 
 
+# ---------------------------------------------------------------------------
+# the conventional comparison strategy (reference planner.py:411-465, 620-713)
+
+
+def plan_conventional(spec: ContractionSpec, layout_a: Layout, layout_b: Layout,
+                      layout_c: Layout, policy: str = "opt") -> EvaluationPlan:
+    """Permute-and-matricize plan: bring operands to C_IJ = A_IK B_KJ form
+    (reference planner.py:411-465, same steps and transposition count).
+
+    policy "opt" replaces single leading-block swaps with transpose op flags
+    and skips the output pre-permute when beta == 0; "naive" materializes
+    every permutation.  This is the baseline the paper measures SBGEMM
+    against; execute_plan runs it on the device (permute kernel + one GEMM)."""
+    if policy not in ("opt", "naive"):
+        raise PlanError(f"unknown conventional policy {policy!r}")
+    cls = classify_indices(spec)
+    plan = EvaluationPlan(spec=spec, layout_a=layout_a, layout_b=layout_b,
+                          layout_c=layout_c, strategy="conventional", steps=[])
+    _modes(spec.labels_a, layout_a)
+    _modes(spec.labels_b, layout_b)
+    if spec.labels_c:
+        _modes(spec.labels_c, layout_c)
+    for name, lay in (("A", layout_a), ("B", layout_b), ("C", layout_c)):
+        if not lay.is_packed():
+            raise PlanError(f"conventional evaluation requires packed {name}")
+    target_a = cls.free_a + cls.contracted
+    target_b = cls.contracted + cls.free_b
+    op_a = op_b = Op.Normal
+    perm_a = perm_b = None
+    if spec.labels_a != target_a:
+        if policy == "opt" and spec.labels_a == cls.contracted + cls.free_a:
+            op_a = Op.Transpose
+        else:
+            perm_a = tuple(spec.labels_a.index(l) for l in target_a)
+            plan.steps.append(PermuteStep("A", perm_a))
+    if spec.labels_b != target_b:
+        if policy == "opt" and spec.labels_b == cls.free_b + cls.contracted:
+            op_b = Op.Transpose
+        else:
+            perm_b = tuple(spec.labels_b.index(l) for l in target_b)
+            plan.steps.append(PermuteStep("B", perm_b))
+    target_c = cls.free_a + cls.free_b
+    c_matches = spec.labels_c == target_c
+    if not c_matches:
+        if policy == "naive" or spec.beta != 0.0:
+            plan.steps.append(PermuteStep("C", tuple(spec.labels_c.index(l) for l in target_c)))
+        plan.steps.append(PermuteStep("C", tuple(target_c.index(l) for l in spec.labels_c)))
+    plan.conventional = ConventionalInfo(
+        free_a=cls.free_a, free_b=cls.free_b, contracted=cls.contracted, op_a=op_a, op_b=op_b,
+        permute_a=perm_a, permute_b=perm_b, c_matches=c_matches, family=kernel_family(cls),
+        policy=policy)
+    plan.predicted_transpositions = sum(1 for st in plan.steps if isinstance(st, PermuteStep))
+    return plan
+
+
+def _execute_conventional(plan, a, b, alpha, beta, c, counters):
+    """Device execution of a conventional plan (reference planner.py:620-713):
+    permute A / B / C into GEMM form with the library's permute kernel, one
+    GEMM (level-2/1 families are the same GEMM with an extent of 1), permute
+    the result back into C."""
+    from .kernels import gemm
+    info = plan.conventional
+    spec = plan.spec
+
+    def note_copy(n_elements):
+        if counters is not None:
+            counters.transpositions += 1
+            counters.bytes_copied += n_elements * c.data.element_size()
+
+    ta = a
+    if info.permute_a is not None:
+        ta = permute_copy(a, info.permute_a)
+        note_copy(ta.layout.size)
+    tb = b
+    if info.permute_b is not None:
+        tb = permute_copy(b, info.permute_b)
+        note_copy(tb.layout.size)
+    ext = {}
+    for labels, lay in ((spec.labels_a, plan.layout_a), (spec.labels_b, plan.layout_b)):
+        ext.update(dict(zip(labels, lay.dims)))
+    mi = prod(ext[l] for l in info.free_a) if info.free_a else 1
+    nj = prod(ext[l] for l in info.free_b) if info.free_b else 1
+    kk = prod(ext[l] for l in info.contracted) if info.contracted else 1
+    target_c = info.free_a + info.free_b
+    if info.c_matches:
+        cbuf = c
+    else:
+        cbuf = DenseTensor.zeros(Layout.packed([ext[l] for l in target_c] or [1]),
+                                 dtype=c.dtype, device=c.device)
+        if beta != 0.0 or info.policy == "naive":
+            perm_in = tuple(spec.labels_c.index(l) for l in target_c)
+            permute_into(c, perm_in, cbuf)
+            note_copy(cbuf.layout.size)
+    lda = kk if info.op_a is Op.Transpose else mi
+    ldb = nj if info.op_b is Op.Transpose else kk
+    gemm(info.op_a, info.op_b, mi, nj, kk, alpha, ta.data, lda, tb.data, ldb, beta,
+         cbuf.data, mi)
+    if counters is not None:
+        fam = info.family.lower()
+        counters.kernel_calls[fam] = counters.kernel_calls.get(fam, 0) + 1
+    if not info.c_matches:
+        perm_out = tuple(target_c.index(l) for l in spec.labels_c)
+        permute_into(cbuf, perm_out, c)
+        note_copy(c.layout.size)
+
+
 def _storage_overlap(x, y) -> bool:
     if x.device != y.device:
         return False
@@ -400,6 +526,9 @@ def execute_plan(plan: EvaluationPlan, a: DenseTensor, b: DenseTensor,
     _check_tensor(plan.layout_c, c, "C")
     if _storage_overlap(c.data, a.data) or _storage_overlap(c.data, b.data):
         raise PlanError("C must not alias A or B")
+    if plan.strategy == "conventional":
+        _execute_conventional(plan, a, b, alpha, beta, c, counters)
+        return
     if plan.strategy not in ("flattened-gemm", "strided-batched", "nested-batched",
                              "extended-batched"):
         raise PlanError(f"strategy {plan.strategy!r} is not executed by this backend")

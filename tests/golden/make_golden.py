@@ -21,7 +21,12 @@ Everything is produced by calling the unmodified reference package
                      (test_kernels.py:12-135) and strided variants;
 * hooi.npz        -- hooi() results (factors, core, fit history) on the
                      reference's Tucker test tensors (test_tucker.py:54-94,
-                     test_acceptance.py:182-201).
+                     test_acceptance.py:182-201);
+* conventional.*  -- plan_conventional plans (steps, ops, transposition count)
+                     and contract_conventional outputs + counters for all 36
+                     (2,3) cases, both policies, beta = 0 and != 0
+                     (planner.py:411-465, 620-713; reference.py:54-63).
+                     ``--only conventional`` regenerates just these.
 
 The fixtures are small (<1 MB) and committed; this script is committed next to
 them so they can be regenerated.
@@ -44,8 +49,9 @@ from sbtensor.kernels import Op  # noqa: E402
 from sbtensor.layout import DenseTensor, Layout  # noqa: E402
 from sbtensor.notation import ContractionSpec  # noqa: E402
 from sbtensor.planner import (BatchedStep, FlattenStep, GemmStep, LoopStep,  # noqa: E402
-                              enumerate_cases, execute_plan, plan_single_mode,
-                              render_plan, resolved_kernel_args)
+                              PermuteStep, enumerate_cases, execute_plan, plan_conventional,
+                              plan_single_mode, render_plan, resolved_kernel_args)
+from sbtensor.reference import contract_conventional  # noqa: E402
 from sbtensor.tucker import hooi, tucker_core, tucker_reconstruct  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -287,8 +293,58 @@ def make_hooi(rng):
     return arrays, index
 
 
+def make_conventional(rng):
+    arrays = {}
+    index = []
+    for case in enumerate_cases(2, 3):
+        for policy in ("opt", "naive"):
+            for rep in range(2):
+                ext = {l: int(rng.integers(2, 8)) for l in "mnpk"}
+                alpha = float(rng.uniform(-2, 2))
+                beta = float(rng.uniform(-2, 2)) if rep else 0.0
+                spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c,
+                                       alpha=alpha, beta=beta)
+                la = Layout.packed([ext[l] for l in spec.labels_a])
+                lb = Layout.packed([ext[l] for l in spec.labels_b])
+                lc = Layout.packed([ext[l] for l in spec.labels_c])
+                plan = plan_conventional(spec, la, lb, lc, policy=policy)
+                info = plan.conventional
+                a = DenseTensor.from_array(rng.uniform(-1, 1, la.dims))
+                b = DenseTensor.from_array(rng.uniform(-1, 1, lb.dims))
+                c = DenseTensor.from_array(rng.uniform(-1, 1, lc.dims))
+                key = f"{case.case_id}_{policy}_{rep}"
+                arrays[key + "_a"] = a.data.copy()
+                arrays[key + "_b"] = b.data.copy()
+                arrays[key + "_c0"] = c.data.copy()
+                counters = contract_conventional(spec, a, b, alpha, beta, c, policy=policy)
+                arrays[key + "_c"] = c.data.copy()
+                index.append({
+                    "key": key, "case_id": case.case_id, "policy": policy,
+                    "a": "".join(spec.labels_a), "b": "".join(spec.labels_b),
+                    "c": "".join(spec.labels_c), "ext": ext, "alpha": alpha, "beta": beta,
+                    "steps": [[st.tensor, list(st.perm)] for st in plan.steps
+                              if isinstance(st, PermuteStep)],
+                    "predicted_transpositions": plan.predicted_transpositions,
+                    "op_a": info.op_a.value, "op_b": info.op_b.value,
+                    "permute_a": None if info.permute_a is None else list(info.permute_a),
+                    "permute_b": None if info.permute_b is None else list(info.permute_b),
+                    "c_matches": info.c_matches, "family": info.family,
+                    "transpositions": counters.transpositions,
+                    "kernel_calls": counters.kernel_calls})
+    return arrays, index
+
+
 def main():
     rng = np.random.default_rng(20260824)
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "conventional":
+        meta = {"reference": REF, "sbtensor_version": sbtensor.__version__,
+                "backend": sbtensor.active_backend(), "numpy": np.__version__}
+        arrays, index = make_conventional(np.random.default_rng(1606))
+        np.savez_compressed(OUT / "conventional.npz", **arrays)
+        (OUT / "conventional.json").write_text(
+            json.dumps({"meta": meta, "records": index}, indent=0))
+        print("wrote conventional fixtures to", OUT)
+        return
     meta = {"reference": REF, "sbtensor_version": sbtensor.__version__,
             "backend": sbtensor.active_backend(), "numpy": np.__version__}
     plans = make_plans(rng)

@@ -31,7 +31,8 @@ def raw(rep):
 
 def main():
     out_md = Path(sys.argv[1])
-    traffic_path = Path("profiles/ncu_traffic.json")
+    import os
+    traffic_path = Path(os.environ.get("NCU_TRAFFIC_JSON", "profiles/ncu_traffic.json"))
     traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
     lines = [f"# ncu --set full captures ({out_md.stem})", "",
              "`ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 2 -c 1`"

@@ -10,7 +10,11 @@ import threading
 from ctypes import c_double, c_float, c_int, c_int64, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libsbt200.so"
+import os
+
+# SBT_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = Path(os.environ.get("SBT_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libsbt200.so")
 
 SBT_OK = 0
 SBT_EINVAL = -1

@@ -64,9 +64,11 @@ constexpr int kGroupWarps = 4;
 // is the deeper one; a smaller BK gives more, finer slots in flight.
 // BB: the converted slot also holds A_hi (the converter re-lays the dense raw
 // A box into the swizzled MN-major atom), so it is 3 operand halves wide.
-// BNT: tile width (N of the MMA): 256, or 128 for N = 128 problems (each CTA
-// then holds 64 columns of B; the 2 x 128 TMEM columns also leave room for
-// double-buffered split accumulators).
+// BNT: tile width (N of the MMA): 256, or 128 / 64 / 32 for narrow problems
+// (each CTA holds BNT/2 columns of B; narrow accumulators leave TMEM room for
+// double-buffered split accumulators).  BNT = 32 serves the rank-32 Tucker
+// products (M' = 262144, N = 32), which are HBM-bound: the MMA's shared-memory
+// reads per flop grow as N shrinks, but the tile still outruns HBM.
 template <int BK, bool BB = false, int BNT = 256>
 struct Geo {
   static constexpr int A_BYTES = 128 * BK * 4;               // A half (128 rows)
@@ -86,7 +88,7 @@ struct Geo {
       RAW_SLOTS * SLOT_BYTES + LO_SLOTS * LO_SLOT_BYTES + EPI_BYTES + 1024 + 512;
   static constexpr uint32_t TX = SLOT_BYTES;                 // raw A + raw B per K-block
   static constexpr int NV = SLOT_BYTES / 16 / 128;           // float4 per converter thread
-  static_assert(NV % 4 == 0, "converter chunks");
+  static_assert(SLOT_BYTES % (16 * 128) == 0, "converter chunks");
   static_assert(RAW_SLOTS <= 16, "barrier area");
 };
 
@@ -165,6 +167,7 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   const int64_t nbatch = BB ? (p.batch + 3) / 4 : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
   using Gm = Geo<BK, BB, BNT>;
   constexpr int HNT = BNT / 2;  // B columns per CTA
+  static_assert(B_K || HNT >= 32, "MN-major B needs 32-column atoms");
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
   constexpr int LO_SLOT_BYTES = Gm::LO_SLOT_BYTES;
@@ -322,12 +325,14 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       const uint32_t raw = ptx::smem_addr(raw_ring + s * SLOT_BYTES);
       constexpr int NV = Gm::NV;  // float4 chunks per thread (A and B halves)
 #pragma unroll
-      for (int h = 0; h < ((p_prefetch >> 9) & 1 ? 0 : NV / 4); ++h) {
+      for (int h = 0; h < ((p_prefetch >> 9) & 1 ? 0 : (NV + 3) / 4); ++h) {
         float4 v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = ptx::lds_v4(raw + (ct + (h * 4 + i) * 128) * 16);
+        for (int i = 0; i < 4; ++i)
+          if (h * 4 + i < NV) v[i] = ptx::lds_v4(raw + (ct + (h * 4 + i) * 128) * 16);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          if (h * 4 + i >= NV) continue;
           uint32_t off = (ct + (h * 4 + i) * 128) * 16;
           if (BB && (h * 4 + i) * 128 < Gm::A_BYTES / 16) {  // chunk lies in the A half
             // dense [k][m8][b4] A chunk -> 32 B-atom swizzle (k row % 4 XOR granule)

@@ -194,11 +194,11 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
       p, ta, tb, tcm, tiles_m, tiles_n, total, f, prefetch);
   note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
                  : (f.fm || f.fn)
-                     ? (BNT == 128 ? (SPLIT ? "tc_tf32x3_pair_fold_n128_splitacc"
-                                            : "tc_tf32x3_pair_fold_n128")
-                                   : (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold"))
-                     : (BNT == 128 ? (SPLIT ? "tc_tf32x3_pair_n128_splitacc" : "tc_tf32x3_pair_n128")
-                                   : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma")));
+                     ? (BNT < 256 ? (SPLIT ? "tc_tf32x3_pair_fold_narrow_splitacc"
+                                           : "tc_tf32x3_pair_fold_narrow")
+                                  : (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold"))
+                     : (BNT < 256 ? (SPLIT ? "tc_tf32x3_pair_narrow_splitacc" : "tc_tf32x3_pair_narrow")
+                                  : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma")));
   return 1;
 }
 
@@ -233,10 +233,25 @@ static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream,
 template <bool SPLIT, int BNT>
 static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
                           const tf32tma::Fold& f) {
-  if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f);
-  if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT, BNT>(p, s, f);
-  if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
-  return launch_tf32tma_cfg<false, false, SPLIT, BNT>(p, s, f);
+  if constexpr (BNT < 64) {  // narrow tiles: B must be K-major (16-column halves)
+    if (bm != 1) return 0;
+    return am == 1 ? launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f)
+                   : launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
+  } else {
+    if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f);
+    if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT, BNT>(p, s, f);
+    if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
+    return launch_tf32tma_cfg<false, false, SPLIT, BNT>(p, s, f);
+  }
+}
+
+template <bool SPLIT>
+static int launch_tf32tma_w(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
+                            const tf32tma::Fold& f) {
+  if (f.ntot <= 32) return launch_tf32tma<SPLIT, 32>(p, am, bm, s, f);
+  if (f.ntot <= 64) return launch_tf32tma<SPLIT, 64>(p, am, bm, s, f);
+  if (f.ntot < 192) return launch_tf32tma<SPLIT, 128>(p, am, bm, s, f);
+  return launch_tf32tma<SPLIT, 256>(p, am, bm, s, f);
 }
 
 template <int BN>
@@ -368,7 +383,12 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
       const int qa = a_major(q), qb = b_major(q);
       if (!qa || !qb) continue;
       const tf32tma::Fold f = variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q);
-      const bool ok = variant == 4 || (f.mtot >= 256 && f.ntot >= 96);
+      // narrow N (< 96) only pays off for many M rows in total (HBM-bound
+      // skinny products: rank-r Tucker mode products)
+      const int64_t rows = f.mtot * ((f.fm == 1 || f.fn == 1) ? 1 : q.batch) *
+                           ((f.fm == 2 || f.fn == 2) ? 1 : q.batch2);
+      const bool ok = variant == 4 ||
+                      (f.mtot >= 256 && (f.ntot >= 96 || (f.ntot >= 16 && rows >= 8192 && qb == 1)));
       if (ok && (!found || f.mtot > bf.mtot || (f.mtot == bf.mtot && f.ntot > bf.ntot))) {
         best = q; bf = f; ba = qa; bb = qb; found = true;
       }
@@ -376,11 +396,8 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
     if (found) {
       static const int split_env = env_int("SBT_TC_SPLITACC", -1);
       const bool split = split_env < 0 ? (best.k > 512) : (split_env != 0);
-      const bool n128 = bf.ntot < 192;
-      const int rc = split ? (n128 ? launch_tf32tma<true, 128>(best, ba, bb, stream, bf)
-                                   : launch_tf32tma<true, 256>(best, ba, bb, stream, bf))
-                           : (n128 ? launch_tf32tma<false, 128>(best, ba, bb, stream, bf)
-                                   : launch_tf32tma<false, 256>(best, ba, bb, stream, bf));
+      const int rc = split ? launch_tf32tma_w<true>(best, ba, bb, stream, bf)
+                           : launch_tf32tma_w<false>(best, ba, bb, stream, bf);
       if (rc != 0) return rc;
     }
   }

@@ -679,3 +679,23 @@ def test_batch_fold_into_m_or_n(shape):
                   host(a), host(b), want)
     assert kern.startswith("tc_tf32x3_pair_fold"), kern
     assert naive.max_rel_err(host(c), want) <= TOL[torch.float32]
+
+
+@pytest.mark.parametrize("m,n,k,P", [(16384, 32, 256, 1), (8192, 48, 100, 1), (12000, 20, 64, 1),
+                                     (512, 32, 512, 40)])
+def test_narrow_tiles_for_skinny_products(m, n, k, P):
+    """Rank-r style products (long M', N <= 64, K-major B) run on the CTA-pair
+    kernel with 32/64-wide tiles (batch folded into M when B is shared)."""
+    rng = np.random.default_rng(m + n)
+    ha = rng.uniform(-1, 1, m * k * P)
+    hb = rng.uniform(-1, 1, k * n)
+    a, b = dev(ha, torch.float32), dev(hb, torch.float32)
+    c = torch.zeros(m * n * P, dtype=torch.float32, device="cuda")
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.0, a, m, m * k, b, k, 0, 0.0, c, m, m * n,
+                                 P)
+    assert _lib.last_kernel().startswith("tc_tf32x3_pair"), _lib.last_kernel()
+    A = host(a).reshape(P, k, m).transpose(0, 2, 1)
+    B = host(b).reshape(n, k).T
+    want = A @ B
+    got = host(c).reshape(P, n, m).transpose(0, 2, 1)
+    assert naive.max_rel_err(got, want) <= TOL[torch.float32]

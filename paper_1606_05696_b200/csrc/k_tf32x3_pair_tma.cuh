@@ -76,7 +76,12 @@ struct Geo {
   static constexpr int OP_BYTES = A_BYTES;
   static constexpr int SLOT_BYTES = A_BYTES + B_BYTES;       // raw A half + raw B half
   static constexpr int LO_SLOT_BYTES = SLOT_BYTES + (BB ? A_BYTES : 0);
-  static constexpr int LO_SLOTS = BK == 32 ? 2 : 4;
+  // The lo ring bounds how far conversion runs ahead of the MMAs: a lo slot
+  // cycles through MMA retire -> commit -> converter -> full barrier (both
+  // CTAs) -> MMA issue, ~2.4K cycles measured (SBT_TRACE).  Wide tiles spend
+  // 1536 cycles of MMA per K-block, so 2 slots cover it; narrow tiles need
+  // more (e.g. 192 cycles per K-block at BNT = 32).
+  static constexpr int LO_SLOTS = (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? 3 : 5);
   // epilogue staging for the TMA-store epilogue: 2 x (128 rows x 32 columns)
   static constexpr int EPI_BYTES = BB ? 0 : 2 * 128 * 32 * 4;
   // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles
@@ -89,7 +94,8 @@ struct Geo {
   static constexpr uint32_t TX = SLOT_BYTES;                 // raw A + raw B per K-block
   static constexpr int NV = SLOT_BYTES / 16 / 128;           // float4 per converter thread
   static_assert(SLOT_BYTES % (16 * 128) == 0, "converter chunks");
-  static_assert(RAW_SLOTS <= 16, "barrier area");
+  static_assert(RAW_SLOTS <= 16 && LO_SLOTS <= 16, "barrier area");
+  static_assert(RAW_SLOTS >= 3, "TMA depth");
 };
 
 // Debug timeline (SBT_TRACE builds only): per-event clock64 stamps of pair 0.
@@ -537,8 +543,10 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       }
     }
     }  // direct-store epilogue
-  } else if (warp == 13 && rank == 0 && lane == 0) {
+  } else if (warp == 13 && rank == 0) {
     // -------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop (waits and descriptor math are
+    // warp-uniform); one elected lane issues the MMAs and commits.
     constexpr uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);
     // K-major: rows of BK*4 bytes (SW128 for BK=32, SW64 for BK=16), 8-row
     // groups at SBO = 8*BK*4, K=8 step = 32 B inside the row.
@@ -569,21 +577,28 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         const uint32_t b_lo = a_lo + Gm::A_BYTES;
         // BB: A_hi is the converter's swizzled copy, not the dense raw box
         const uint32_t a_raw = BB ? a_lo + Gm::SLOT_BYTES : b_raw - Gm::A_BYTES;
+        if (ptx::elect_one_sync()) {
 #pragma unroll
-        for (int j = 0; j < BK / 8; ++j) {
-          const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t dbr = ptx::umma_desc(b_raw + j * b_step, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
-          const uint32_t first = (kb | j) ? 1u : 0u;
-          ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, first);
-          ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
-          ptx::mma2_tf32_ss(d_main, dar, dbr, idesc, SPLIT_ACC ? first : 1u);
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dbr = ptx::umma_desc(b_raw + j * b_step, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
+            const uint32_t first = (kb | j) ? 1u : 0u;
+            ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, first);
+            ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
+            ptx::mma2_tf32_ss(d_main, dar, dbr, idesc, SPLIT_ACC ? first : 1u);
+          }
+          ptx::tc_commit2_mc(&raw_empty[s], 0x3);
+          ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
         }
-        ptx::tc_commit2_mc(&raw_empty[s], 0x3);
-        ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
+        __syncwarp();
+#ifdef SBT_TRACE
+        if (blockIdx.x < 2 && it < 4096) g_trace[7][it] = clock64();  // issue done (rank-1 row 3)
+#endif
       }
-      ptx::tc_commit2_mc(&acc_full[b], 0x3);
+      if (ptx::elect_one_sync()) ptx::tc_commit2_mc(&acc_full[b], 0x3);
+      __syncwarp();
     }
   }
 

@@ -271,6 +271,18 @@ __device__ __forceinline__ void mma2_tf32_ss(uint32_t d_tmem, uint64_t adesc, ui
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): used to issue tcgen05.mma /
+// commit from a warp-uniform loop, so descriptors stay in uniform registers
+// (a lane-0-only region makes the compiler wrap every MMA in an R2UR
+// "waterfall" loop: ~80 cycles per MMA, measured).
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- descriptors -------------------------------------------------------------
 // UMMA shared-memory descriptor (sm100 version bit).
 //   K-major, SWIZZLE_128B (layout 2): 8-row x 128 B atoms (16 B chunks XOR row%8),

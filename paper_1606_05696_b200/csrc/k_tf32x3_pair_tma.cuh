@@ -230,8 +230,10 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   const int64_t n_iter = my_tiles * nkb;
 
   if (warp == 12) {
-    if (lane == 0) {
+    {
       // -------------------------------------------------------- TMA producer
+      // warp-uniform loop (coordinates in uniform registers); one elected lane
+      // issues the TMA boxes
       const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
       // Per-tile TMA coordinates, decoded once per tile (64-bit divisions are
       // slow on the single producer thread)
@@ -294,7 +296,9 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           if (pf_tile < total) pf_c = decode(pf_tile);
         }
       };
-      for (int i = 0; i < pfd; ++i) prefetch_next();
+      if (ptx::elect_one_sync())
+        for (int i = 0; i < pfd; ++i) prefetch_next();
+      __syncwarp();
       int64_t g = 0;
       for (int64_t t = pair; t < total; t += npairs) {
         const Coord c = decode(t);
@@ -302,14 +306,17 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
           const uint32_t s = uint32_t(g % RAW_SLOTS);
           ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
           TRACE(0, int(g));
-          if (pfd > 0) prefetch_next();
           uint8_t* st = raw_ring + s * SLOT_BYTES;
-          if (dbg_no_tma) {
-            ptx::mbar_arrive(&raw_full[s]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
-            boxes(c, kb * BK, st, &raw_full[s], std::false_type{});
+          if (ptx::elect_one_sync()) {
+            if (pfd > 0) prefetch_next();
+            if (dbg_no_tma) {
+              ptx::mbar_arrive(&raw_full[s]);
+            } else {
+              ptx::mbar_arrive_expect_tx(&raw_full[s], Gm::TX);
+              boxes(c, kb * BK, st, &raw_full[s], std::false_type{});
+            }
           }
+          __syncwarp();
         }
       }
     }

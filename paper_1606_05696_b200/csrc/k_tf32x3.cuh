@@ -188,8 +188,9 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
       if (kb + 2 < nkb) load(kb + 2, ra0, rb0);
       produce(kb + 1, ra1, rb1);
     }
-  } else if (lane == 0) {
+  } else {
     // ------------------------------------------------------------ MMA issuer
+    // warp-uniform loop, one elected lane issues (descriptors stay uniform)
     constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, !A_K, !B_K);
     // per-MMA (K = 8) descriptor advance: 32 B inside a K-major row, or one
     // 8-deep K group (SBO) for MN-major
@@ -212,21 +213,25 @@ tf32x3_gemm_kernel(GemmParams<float> p, int64_t tiles_m, int64_t tiles_n) {
       const uint32_t a_lo = a_hi + C_::A_BYTES;
       const uint32_t b_hi = a_lo + C_::A_BYTES;
       const uint32_t b_lo = b_hi + C_::B_BYTES;
+      if (ptx::elect_one_sync()) {
 #pragma unroll
-      for (int j = 0; j < BK / 8; ++j) {
-        const uint64_t dah = ptx::umma_desc(a_hi + j * a_step, a_lbo, a_sbo, a_lay);
-        const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
-        const uint64_t dbh = ptx::umma_desc(b_hi + j * b_step, b_lbo, b_sbo, b_lay);
-        const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
-        const uint32_t acc = (kb | j) ? 1u : 0u;
-        const uint32_t small = tmem_base + C_::ACC_COLS;
-        ptx::mma_tf32_ss(small, dal, dbh, idesc, acc);  // small terms apart
-        ptx::mma_tf32_ss(small, dah, dbl, idesc, 1u);
-        ptx::mma_tf32_ss(tmem_base, dah, dbh, idesc, acc);
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint64_t dah = ptx::umma_desc(a_hi + j * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = ptx::umma_desc(b_hi + j * b_step, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
+          const uint32_t acc = (kb | j) ? 1u : 0u;
+          const uint32_t small = tmem_base + C_::ACC_COLS;
+          ptx::mma_tf32_ss(small, dal, dbh, idesc, acc);  // small terms apart
+          ptx::mma_tf32_ss(small, dah, dbl, idesc, 1u);
+          ptx::mma_tf32_ss(tmem_base, dah, dbh, idesc, acc);
+        }
+        ptx::tc_commit(&empty[s]);  // stage reusable once these MMAs retire
       }
-      ptx::tc_commit(&empty[s]);  // stage reusable once these MMAs retire
+      __syncwarp();
     }
-    ptx::tc_commit(accf);  // accumulator complete
+    if (ptx::elect_one_sync()) ptx::tc_commit(accf);  // accumulator complete
+    __syncwarp();
   }
 
   // ------------------------------------------------------------ epilogue

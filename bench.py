@@ -555,25 +555,34 @@ def run_config(args):
         work = build_sets(cases, n, dtype, "cuda", 2, seed=7)
         per = {}
         tot_sb = tot_conv = 0.0
+        tot_gemv = 0.0
         for cid, plan, a, b, c in work:
             conv = sbt.plan_conventional(plan.spec, a.layout, b.layout, c.layout, policy="opt")
+            gv = sbt.plan_batched_gemv(plan.spec, a.layout, b.layout, c.layout)
             ms_sb = _time_steps(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), args.steps,
                                 args.warmup)
             ms_cv = _time_steps(lambda: execute_plan(conv, a, b, 1.0, 0.0, c), args.steps,
                                 args.warmup)
+            ms_gv = _time_steps(lambda: execute_plan(gv, a, b, 1.0, 0.0, c), max(1, args.steps // 2),
+                                1)
             tot_sb += ms_sb
             tot_conv += ms_cv
+            tot_gemv += ms_gv
             per[cid] = {"sbgemm_ms": round(ms_sb, 4), "conventional_ms": round(ms_cv, 4),
+                        "batched_gemv_ms": round(ms_gv, 4),
                         "transpositions": conv.predicted_transpositions,
-                        "speedup": round(ms_cv / ms_sb, 2)}
+                        "speedup": round(ms_cv / ms_sb, 2),
+                        "speedup_vs_gemv": round(ms_gv / ms_sb, 2)}
         fl = 2.0 * n ** 4 * len(work)
-        line = {"metric": "transpose-free SBGEMM vs conventional permute+GEMM (36 cases)",
+        line = {"metric": "transpose-free SBGEMM vs conventional permute+GEMM (36 cases); "
+                          "batched GEMV as the third strategy",
                 "value": round(tot_conv / tot_sb, 3), "unit": "x (conventional time / "
                 "transpose-free time)",
                 "config": {"workload": f"36-case sweep n={n} {args.dtype}, device, "
                                        "conventional policy opt",
                            "sbgemm_gflops": round(fl / (tot_sb * 1e-3) / 1e9, 1),
-                           "conventional_gflops": round(fl / (tot_conv * 1e-3) / 1e9, 1)},
+                           "conventional_gflops": round(fl / (tot_conv * 1e-3) / 1e9, 1),
+                           "batched_gemv_gflops": round(fl / (tot_gemv * 1e-3) / 1e9, 1)},
                 "per_case": per}
     else:
         raise SystemExit(f"unknown config {args.config}")

@@ -20,6 +20,7 @@
 #include "k_dmma.cuh"
 #include "k_small.cuh"
 #include "k_small_dmma.cuh"
+#include "k_gemv.cuh"
 #include "sbt_tma.cuh"
 
 namespace sbt {
@@ -533,7 +534,7 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
   // on 16 / 4 / 1 CTAs; fp32 tiles are larger and faster, so only very long
   // reductions split
   const int64_t min_k = sizeof(T) == 8 ? 256 : 16384, min_chunk = sizeof(T) == 8 ? 64 : 4096;
-  if (p.batch != 1 || p.batch2 != 1 || p.k < min_k) return 0;
+  if (p.batch != 1 || p.batch2 != 1 || p.k < min_k || p.m == 1 || p.n == 1) return 0;
   const int64_t tiles = ceil_div(p.m, 128) * ceil_div(p.n, 128);
   if (tiles >= kNumSMs / 2) return 0;
   int64_t S = (2 * kNumSMs) / tiles;
@@ -624,9 +625,36 @@ static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
   return launch_chunked<T>(p, stream);
 }
 
+// GEMV-shaped calls (one of M, N is 1): bandwidth-bound streaming kernels
+template <typename T>
+static int try_gemv(const GemmParams<T>& p0, cudaStream_t stream) {
+  if (p0.n != 1 && p0.m != 1) return 0;
+  const GemmParams<T> p = p0.n == 1 ? p0 : transposed(p0);
+  if (p.n != 1) return 0;
+  if (p.acs == 1 && p.ars != 1) {
+    const int64_t warps = p.m * p.batch * p.batch2;
+    const int64_t blocks = ceil_div(warps, gemv::kThreads / 32);
+    const int64_t grid = blocks < int64_t(kNumSMs) * 16 ? blocks : int64_t(kNumSMs) * 16;
+    gemv::gemv_dot_kernel<T><<<unsigned(grid), gemv::kThreads, 0, stream>>>(p);
+    note_launch(sizeof(T) == 4 ? "gemv_dot_f32" : "gemv_dot_f64");
+  } else {
+    const int64_t nblk = ceil_div(p.m, gemv::kThreads);
+    const int64_t work = nblk * p.batch * p.batch2;
+    const int64_t grid = work < int64_t(kNumSMs) * 16 ? work : int64_t(kNumSMs) * 16;
+    gemv::gemv_rows_kernel<T><<<unsigned(grid), gemv::kThreads, 0, stream>>>(p, nblk);
+    note_launch(sizeof(T) == 4 ? "gemv_rows_f32" : "gemv_rows_f64");
+  }
+  return 1;
+}
+
 template <typename T>
 static int launch_gemm_core(const GemmParams<T>& p, cudaStream_t stream) {
   const int ov = kernel_override();
+  if (ov == 0) {
+    const int rc = try_gemv<T>(p, stream);
+    if (rc < 0) return rc;
+    if (rc == 1) return 0;
+  }
   if (ov == 0 || ov == 3) {
     const int rc = try_small<T>(p, stream, ov == 3);
     if (rc < 0) return rc;

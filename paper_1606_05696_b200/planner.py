@@ -86,6 +86,15 @@ class BatchedStep:
 
 
 @dataclass(frozen=True)
+class GemvBatchStep:
+    loop_labels: tuple
+    matrix: str                 # tensor acting as the GEMV matrix
+    op: Op
+    v_label: str                # output mode of each GEMV
+    k_label: str
+
+
+@dataclass(frozen=True)
 class PermuteStep:
     tensor: str
     perm: tuple
@@ -451,6 +460,82 @@ def plan_conventional(spec: ContractionSpec, layout_a: Layout, layout_b: Layout,
     return plan
 
 
+def _eff_find(eff, label):
+    for i, mode in enumerate(eff):
+        if mode.label == label:
+            return i
+    return -1
+
+
+def _eff_stride(eff, label):
+    i = _eff_find(eff, label)
+    return eff[i].stride if i >= 0 else None
+
+
+def plan_batched_gemv(spec: ContractionSpec, layout_a: Layout, layout_b: Layout,
+                      layout_c: Layout) -> EvaluationPlan:
+    """Looped-GEMV evaluation (reference planner.py:374-404): no copies, lower
+    arithmetic intensity -- the third strategy of the paper's exceptional-case
+    comparison (Fig. 10).  Executed on the device as ONE batched
+    GEMV launch (loop modes become the grid's batch modes)."""
+    cls = classify_indices(spec)
+    if len(cls.contracted) != 1:
+        raise UnsupportedContractionError("batched-gemv planning is single-mode only")
+    k_label = cls.contracted[0]
+    plan = plan_single_mode(spec, layout_a, layout_b, layout_c)  # squeeze / flatten
+    ea, eb, ec = plan.eff["A"], plan.eff["B"], plan.eff["C"]
+    if not ec:
+        raise PlanError("scalar output has no batched-gemv form")
+    c1 = ec[0].label
+    first = "A" if _eff_find(ea, c1) >= 0 else "B"
+    ex = ea if first == "A" else eb
+    if ex[0].label == k_label:
+        v_label, op = c1, Op.Transpose
+    elif ex[0].label == c1:
+        v_label, op = c1, Op.Normal
+    else:
+        v_label, op = ex[0].label, Op.Normal
+    loops = tuple(m.label for m in ec if m.label != v_label)
+    gplan = EvaluationPlan(spec=spec, layout_a=layout_a, layout_b=layout_b,
+                           layout_c=layout_c, strategy="batched-gemv",
+                           steps=[st for st in plan.steps if isinstance(st, FlattenStep)],
+                           eff=plan.eff)
+    gplan.steps.append(GemvBatchStep(loop_labels=loops, matrix=first, op=op,
+                                     v_label=v_label, k_label=k_label))
+    return gplan
+
+
+def _execute_gemv(plan, a, b, alpha, beta, c, counters):
+    """Device execution of a batched-GEMV plan: every GEMV of the reference's
+    loop (planner.py:584-617) in one strided batched launch with n = 1."""
+    eff = plan.eff
+    ea, eb, ec = eff["A"], eff["B"], eff["C"]
+    st = plan.steps[-1]
+    ex, ey = (ea, eb) if st.matrix == "A" else (eb, ea)
+    bx, by = (a, b) if st.matrix == "A" else (b, a)
+    extent = {mo.label: mo.extent for mo in (*ea, *eb, *ec)}
+    # y[v] = sum_k X[v, k] x[k]  (op only records which X mode is unit stride)
+    m, kk = extent[st.v_label], extent[st.k_label]
+    ars, acs = _eff_stride(ex, st.v_label), _eff_stride(ex, st.k_label)
+    brs, crs = _eff_stride(ey, st.k_label), _eff_stride(ec, st.v_label)
+    loops = [(extent[l], _eff_stride(ex, l) or 0, _eff_stride(ey, l) or 0,
+              _eff_stride(ec, l) or 0) for l in st.loop_labels]
+    inner = loops[-2:]                        # fused into the launch (batch, batch2)
+    outer = loops[:-2]
+    while len(inner) < 2:
+        inner.append((1, 0, 0, 0))
+    (b1, apt, bpt, cpt), (b2, apt2, bpt2, cpt2) = inner
+    for combo in itertools.product(*(range(e) for e, *_ in outer)):
+        ox = sum(i * sx for i, (_, sx, _, _) in zip(combo, outer))
+        oy = sum(i * sy for i, (_, _, sy, _) in zip(combo, outer))
+        oc = sum(i * sc for i, (_, _, _, sc) in zip(combo, outer))
+        core_call(m, 1, kk, alpha, bx.data, ox, ars, acs, apt, by.data, oy, brs, 1, bpt, beta,
+                  c.data, oc, crs, 1, cpt, batch=b1, apt2=apt2, bpt2=bpt2, cpt2=cpt2,
+                  batch2=b2)
+        if counters is not None:
+            counters.kernel_calls["gemv"] = counters.kernel_calls.get("gemv", 0) + 1
+
+
 def _execute_conventional(plan, a, b, alpha, beta, c, counters):
     """Device execution of a conventional plan (reference planner.py:620-713):
     permute A / B / C into GEMM form with the library's permute kernel, one
@@ -528,6 +613,9 @@ def execute_plan(plan: EvaluationPlan, a: DenseTensor, b: DenseTensor,
         raise PlanError("C must not alias A or B")
     if plan.strategy == "conventional":
         _execute_conventional(plan, a, b, alpha, beta, c, counters)
+        return
+    if plan.strategy == "batched-gemv":
+        _execute_gemv(plan, a, b, alpha, beta, c, counters)
         return
     if plan.strategy not in ("flattened-gemm", "strided-batched", "nested-batched",
                              "extended-batched"):

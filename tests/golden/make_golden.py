@@ -48,9 +48,10 @@ from sbtensor import kernels  # noqa: E402
 from sbtensor.kernels import Op  # noqa: E402
 from sbtensor.layout import DenseTensor, Layout  # noqa: E402
 from sbtensor.notation import ContractionSpec  # noqa: E402
-from sbtensor.planner import (BatchedStep, FlattenStep, GemmStep, LoopStep,  # noqa: E402
-                              PermuteStep, enumerate_cases, execute_plan, plan_conventional,
-                              plan_single_mode, render_plan, resolved_kernel_args)
+from sbtensor.planner import (BatchedStep, FlattenStep, GemmStep, GemvBatchStep,  # noqa: E402
+                              LoopStep, PermuteStep, enumerate_cases, execute_plan,
+                              plan_batched_gemv, plan_conventional, plan_single_mode,
+                              render_plan, resolved_kernel_args)
 from sbtensor.reference import contract_conventional  # noqa: E402
 from sbtensor.tucker import hooi, tucker_core, tucker_reconstruct  # noqa: E402
 
@@ -331,6 +332,37 @@ def make_conventional(rng):
                     "c_matches": info.c_matches, "family": info.family,
                     "transpositions": counters.transpositions,
                     "kernel_calls": counters.kernel_calls})
+    # batched-GEMV strategy (planner.py:374-404, 584-617)
+    for case in enumerate_cases(2, 3):
+        for rep in range(2):
+            ext = {l: int(rng.integers(2, 8)) for l in "mnpk"}
+            alpha = float(rng.uniform(-2, 2))
+            beta = float(rng.uniform(-2, 2)) if rep else 0.0
+            spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+            la = Layout.packed([ext[l] for l in spec.labels_a])
+            lb = Layout.packed([ext[l] for l in spec.labels_b])
+            lc = Layout.packed([ext[l] for l in spec.labels_c])
+            plan = plan_batched_gemv(spec, la, lb, lc)
+            step = plan.steps[-1]
+            assert isinstance(step, GemvBatchStep)
+            a = DenseTensor.from_array(rng.uniform(-1, 1, la.dims))
+            b = DenseTensor.from_array(rng.uniform(-1, 1, lb.dims))
+            c = DenseTensor.from_array(rng.uniform(-1, 1, lc.dims))
+            key = f"gemv_{case.case_id}_{rep}"
+            arrays[key + "_a"] = a.data.copy()
+            arrays[key + "_b"] = b.data.copy()
+            arrays[key + "_c0"] = c.data.copy()
+            execute_plan(plan, a, b, alpha, beta, c)
+            arrays[key + "_c"] = c.data.copy()
+            index.append({
+                "key": key, "case_id": case.case_id, "policy": "batched-gemv",
+                "a": "".join(spec.labels_a), "b": "".join(spec.labels_b),
+                "c": "".join(spec.labels_c), "ext": ext, "alpha": alpha, "beta": beta,
+                "flatten": [[st.tensor, list(st.labels), st.merged] for st in plan.steps
+                            if isinstance(st, FlattenStep)],
+                "gemv": {"loop_labels": list(step.loop_labels), "matrix": step.matrix,
+                         "op": step.op.value, "v_label": step.v_label,
+                         "k_label": step.k_label}})
     return arrays, index
 
 

@@ -13,8 +13,20 @@ from paper_1606_05696_b200.planner import PermuteStep, plan_conventional
 
 
 @pytest.fixture(scope="module")
-def golden_conv():
+def golden_all():
     return load_json("conventional.json")["records"], np.load(GOLDEN / "conventional.npz")
+
+
+@pytest.fixture(scope="module")
+def golden_conv(golden_all):
+    records, arr = golden_all
+    return [r for r in records if r["policy"] != "batched-gemv"], arr
+
+
+@pytest.fixture(scope="module")
+def golden_gemv(golden_all):
+    records, arr = golden_all
+    return [r for r in records if r["policy"] == "batched-gemv"], arr
 
 
 def _plan(rec):
@@ -98,3 +110,62 @@ def test_permute_copy_matches_numpy():
             torch.cuda.synchronize()
             assert transposition_count() == n0 + 1
             np.testing.assert_array_equal(out.to_array(), np.transpose(x, perm))
+
+
+# ------------------------------------------------------------------ batched-GEMV strategy
+
+
+def _gemv_plan(rec):
+    from paper_1606_05696_b200.planner import plan_batched_gemv
+    spec = ContractionSpec(tuple(rec["a"]), tuple(rec["b"]), tuple(rec["c"]))
+    ext = rec["ext"]
+    lays = [Layout.packed([ext[l] for l in labs]) for labs in (rec["a"], rec["b"], rec["c"])]
+    return spec, lays, plan_batched_gemv(spec, *lays)
+
+
+def test_batched_gemv_plans_match_reference(golden_gemv):
+    from paper_1606_05696_b200.planner import FlattenStep, GemvBatchStep
+    records, _ = golden_gemv
+    assert len(records) == 36 * 2
+    for rec in records:
+        _, _, plan = _gemv_plan(rec)
+        assert plan.strategy == "batched-gemv"
+        st = plan.steps[-1]
+        assert isinstance(st, GemvBatchStep)
+        assert {"loop_labels": list(st.loop_labels), "matrix": st.matrix, "op": st.op.value,
+                "v_label": st.v_label, "k_label": st.k_label} == rec["gemv"], rec["key"]
+        assert [[f.tensor, list(f.labels), f.merged] for f in plan.steps
+                if isinstance(f, FlattenStep)] == rec["flatten"], rec["key"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batched_gemv_execution_matches_reference(golden_gemv, dtype):
+    import torch
+
+    from paper_1606_05696_b200 import _lib
+    from paper_1606_05696_b200.layout import DenseTensor
+    from paper_1606_05696_b200.planner import execute_plan
+    from oracle import naive, plan as oplan
+    records, arr = golden_gemv
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    for rec in records:
+        spec, lays, plan = _gemv_plan(rec)
+        key = rec["key"]
+        a = DenseTensor(lays[0], torch.as_tensor(arr[key + "_a"], device="cuda").to(tdt))
+        b = DenseTensor(lays[1], torch.as_tensor(arr[key + "_b"], device="cuda").to(tdt))
+        c = DenseTensor(lays[2], torch.as_tensor(arr[key + "_c0"], device="cuda").to(tdt))
+        n0 = _lib.launch_count()
+        execute_plan(plan, a, b, rec["alpha"], rec["beta"], c)
+        assert _lib.launch_count() - n0 == 1, key      # every GEMV of the loop in one launch
+        assert _lib.last_kernel().startswith("gemv_"), _lib.last_kernel()
+        got = c.data.double().cpu().numpy()
+        if dtype == "float64":
+            want = arr[key + "_c"]
+        else:
+            want = c.data.new_tensor(arr[key + "_c0"]).double().cpu().numpy().copy()
+            oplan.contract(tuple(rec["a"]), tuple(rec["b"]), tuple(rec["c"]), rec["ext"],
+                           a.data.double().cpu().numpy(), b.data.double().cpu().numpy(),
+                           rec["alpha"], rec["beta"], want)
+        assert naive.max_rel_err(got, want) <= tol, key

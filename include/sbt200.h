@@ -126,6 +126,25 @@ int sbt_batched2_core_f32(int64_t m, int64_t n, int64_t k, float alpha,
                           int64_t cpt, int64_t cpt2, int64_t batch, int64_t batch2,
                           void* stream);
 
+/* ---- grouped execution (no reference counterpart: the reference runs its
+        contractions one call at a time).  `count` INDEPENDENT strided batched
+        GEMMs -- no problem's C may overlap another problem's A, B or C -- in
+        as few launches as possible: problems the CTA-pair tcgen05 kernel takes
+        share one persistent launch per kernel configuration (one pipeline
+        fill / drain / tail instead of one per problem); the rest run as
+        single calls.  Each descriptor has the batched2 entry point's meaning
+        (alpha/beta are converted to the buffer type). */
+typedef struct sbt_gemm_desc {
+  int64_t m, n, k;
+  double alpha, beta;
+  const void* a; int64_t oa, ars, acs, apt, apt2;
+  const void* b; int64_t ob, brs, bcs, bpt, bpt2;
+  void* c; int64_t oc, crs, ccs, cpt, cpt2;
+  int64_t batch, batch2;
+} sbt_gemm_desc;
+int sbt_batched_core_group_f32(int count, const sbt_gemm_desc* descs, void* stream);
+int sbt_batched_core_group_f64(int count, const sbt_gemm_desc* descs, void* stream);
+
 /* ---- host-buffer seam: the reference's cores take flat numpy buffers
         (backend.py:29-31).  These copy the touched span of A, B (and C) to the
         device, run the same kernels, copy C back and synchronise. */

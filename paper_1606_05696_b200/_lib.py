@@ -40,6 +40,19 @@ def _batched2_sig(real):
             _I, _I, _I, _I, _I, _P]
 
 
+class GemmDesc(ctypes.Structure):
+    """sbt_gemm_desc (include/sbt200.h): one problem of a grouped call."""
+    _fields_ = [("m", c_int64), ("n", c_int64), ("k", c_int64),
+                ("alpha", c_double), ("beta", c_double),
+                ("a", c_void_p), ("oa", c_int64), ("ars", c_int64), ("acs", c_int64),
+                ("apt", c_int64), ("apt2", c_int64),
+                ("b", c_void_p), ("ob", c_int64), ("brs", c_int64), ("bcs", c_int64),
+                ("bpt", c_int64), ("bpt2", c_int64),
+                ("c", c_void_p), ("oc", c_int64), ("crs", c_int64), ("ccs", c_int64),
+                ("cpt", c_int64), ("cpt2", c_int64),
+                ("batch", c_int64), ("batch2", c_int64)]
+
+
 # every symbol include/sbt200.h declares, with its ctypes signature
 SIGNATURES = {
     "sbt_version": ([], c_int),
@@ -54,6 +67,8 @@ SIGNATURES = {
                         c_int),
     "sbt_permute_f32": ([c_int, ctypes.POINTER(c_int64), _P, ctypes.POINTER(c_int64), _P, _P],
                         c_int),
+    "sbt_batched_core_group_f32": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),
+    "sbt_batched_core_group_f64": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),
     "sbt_gemm_core_f64": (_core_sig(c_double), c_int),
     "sbt_gemm_core_f32": (_core_sig(c_float), c_int),
     "sbt_batched_core_f64": (_batched_sig(c_double), c_int),

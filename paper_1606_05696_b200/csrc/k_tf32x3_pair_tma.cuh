@@ -28,6 +28,13 @@
 // of 4 warps taking alternate K-blocks, so each has two K-blocks of time),
 // 12 TMA producer + TMEM allocator, 13 MMA issuer (leader).
 //
+// Problem sets: the kernel walks the tiles of up to MAXP independent problems
+// (each with its own operands, strides, K-major / MN-major layouts, fold and
+// tensor maps, passed by value in the kernel parameters) in one persistent
+// launch.  A single contraction is MAXP = 1; a group of independent
+// contractions (e.g. the 36-case sweep) shares one pipeline fill, one drain
+// and one tile-quantisation tail instead of paying them per contraction.
+//
 // Batch-blocked A (BB, the exceptional cases, reference kernels.py:179-204):
 // the A operand is unit-stride along the BATCH mode (apt = 1) while C is
 // unit-stride along m.  Each CTA's 128 MMA rows are (4 consecutive batch
@@ -126,6 +133,31 @@ struct Fold {
   int cmode;
 };
 
+// One problem of a set.  Tensor maps first (64-byte aligned).
+struct Problem {
+  CUtensorMap ta, tb, tc;
+  GemmParams<float> p;
+  Fold f;
+  int64_t tiles_m, tiles_n, nbatch;  // tile grid (nbatch: batch units the tiles run over)
+  int64_t tile_begin;                // first global tile index of this problem
+  int a_k, b_k;                      // operand majorness: 1 = K-major
+  int nkb;                           // K-blocks per tile
+  int pad;
+};
+template <int MAXP>
+struct ProblemSet {
+  Problem pr[MAXP];
+  int64_t total;  // tiles over all problems
+  int n;
+};
+
+// problem owning global tile t; `cur` only moves forward (every role walks
+// its tiles in increasing order)
+__device__ __forceinline__ const Problem& locate(const Problem* pr, int n, int64_t t, int& cur) {
+  while (cur + 1 < n && t >= pr[cur + 1].tile_begin) ++cur;
+  return pr[cur];
+}
+
 // BB tiles cover 64 m (32 per CTA) x 4 batch entries; pb is then the batch group
 template <bool BB = false, int BNT = BN>
 __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tiles_n,
@@ -144,12 +176,12 @@ __device__ __forceinline__ Tile tile_of(int64_t t, int64_t tiles_m, int64_t tile
 // dimension x BK k).  K-major: one box (BK k, ROWS mn).  MN-major: ROWS/32 boxes
 // (32 mn, BK k), one per 32-wide MN atom column, each a contiguous slab of BK
 // 128-byte rows.  PREFETCH: the same boxes as L2 prefetches (no smem).
-template <bool KMAJ, int BK, bool PREFETCH = false, int ROWS = 128>
-__device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar,
-                                            int64_t mn0, int64_t k0, int64_t b, int64_t b2,
-                                            bool bcast, bool bcast2) {
+template <int BK, bool PREFETCH = false, int ROWS = 128>
+__device__ __forceinline__ void tma_operand(bool kmaj, const CUtensorMap* tm, uint8_t* dst,
+                                            uint64_t* bar, int64_t mn0, int64_t k0, int64_t b,
+                                            int64_t b2, bool bcast, bool bcast2) {
   const int cb = bcast ? 0 : int(b), cb2 = bcast2 ? 0 : int(b2);
-  if (KMAJ) {
+  if (kmaj) {
     if (PREFETCH) ptx::tma_prefetch_4d(tm, int(k0), int(mn0), cb, cb2);
     else ptx::tma_load_4d(dst, tm, bar, int(k0), int(mn0), cb, cb2);
   } else {
@@ -161,19 +193,14 @@ __device__ __forceinline__ void tma_operand(const CUtensorMap* tm, uint8_t* dst,
   }
 }
 
-template <bool A_K, bool B_K, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256>
+template <int MAXP, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
-                       const __grid_constant__ CUtensorMap tmB,
-                       const __grid_constant__ CUtensorMap tmC, int64_t tiles_m,
-                       int64_t tiles_n, int64_t total, Fold f, int p_prefetch) {
-  static_assert(!(BB && A_K), "batch-blocked A is MN-major");
-  // number of batch units the tile index runs over (BB: groups of 4 entries;
-  // a folded batch mode is not a tile dimension)
-  const int64_t nbatch = BB ? (p.batch + 3) / 4 : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
+tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefetch) {
+  const Problem* __restrict__ prs = ps.pr;
+  const int nprob = ps.n;
+  const int64_t total = ps.total;
   using Gm = Geo<BK, BB, BNT>;
-  constexpr int HNT = BNT / 2;  // B columns per CTA
-  static_assert(B_K || HNT >= 32, "MN-major B needs 32-column atoms");
+  constexpr int HNT = BNT / 2;  // B columns per CTA (MN-major B needs HNT >= 32: host-checked)
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
   constexpr int LO_SLOT_BYTES = Gm::LO_SLOT_BYTES;
@@ -197,7 +224,6 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   const uint32_t rank = ptx::cluster_rank();
   const int64_t pair = blockIdx.x >> 1;
   const int64_t npairs = gridDim.x >> 1;
-  const int nkb = int((p.k + BK - 1) / BK);
   // TMEM: NBUF buffers of (main [+ small]) BNT-column accumulators in 512 columns
   constexpr int ACC_W = (SPLIT_ACC ? 2 : 1) * BNT;
   constexpr int NBUF = 512 / ACC_W >= 2 ? 2 : 1;
@@ -215,9 +241,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
         ptx::mbar_init(&acc_empty[b], 2 * 4);  // one arrival per epilogue warp of each CTA
       }
       ptx::fence_mbarrier_init();
-      ptx::prefetch_tmap(&tmA);
-      ptx::prefetch_tmap(&tmB);
-      if (!BB && f.cmode) ptx::prefetch_tmap(&tmC);
+      for (int i = 0; i < nprob; ++i) {
+        ptx::prefetch_tmap(&prs[i].ta);
+        ptx::prefetch_tmap(&prs[i].tb);
+        if (!BB && prs[i].f.cmode) ptx::prefetch_tmap(&prs[i].tc);
+      }
     }
     __syncwarp();
     ptx::tmem_alloc2(tmem_slot, 512);
@@ -226,23 +254,25 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t my_tiles = (total - pair + npairs - 1) / npairs;
-  const int64_t n_iter = my_tiles * nkb;
 
   if (warp == 12) {
     {
       // -------------------------------------------------------- TMA producer
       // warp-uniform loop (coordinates in uniform registers); one elected lane
       // issues the TMA boxes
-      const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
-      // Per-tile TMA coordinates, decoded once per tile (64-bit divisions are
-      // slow on the single producer thread)
+      // Per-tile TMA coordinates, decoded once per tile
       struct Coord {
+        const Problem* pr;
         int am, ab, ab2, bn, bb, bb2;
       };
-      auto decode = [&](int64_t tile_idx) {
-        const Tile tc = tile_of<BB, BNT>(tile_idx, tiles_m, tiles_n, nbatch);
+      auto decode = [&](int64_t tile_idx, int& cur) {
+        const Problem& P = locate(prs, nprob, tile_idx, cur);
+        const GemmParams<float>& p = P.p;
+        const Fold& f = P.f;
+        const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
+        const Tile tc = tile_of<BB, BNT>(tile_idx - P.tile_begin, P.tiles_m, P.tiles_n, P.nbatch);
         Coord c;
+        c.pr = &P;
         if (BB) {
           c.am = int(tc.m0 + rank * 32); c.ab = int(tc.pb * 4); c.ab2 = a_bc2 ? 0 : int(tc.qb);
           c.bn = int(tc.n0 + rank * HNT); c.bb = b_bc ? 0 : int(tc.pb); c.bb2 = b_bc2 ? 0 : int(tc.qb);
@@ -269,31 +299,33 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       // as L2 prefetches (PF = true, st unused)
       auto boxes = [&](const Coord& c, int k0, uint8_t* st, uint64_t* bar, auto pf) {
         constexpr bool PF = decltype(pf)::value;
+        const CUtensorMap* tmA = &c.pr->ta;
         if (BB) {  // four dense (4 batch, 8 m, BK k) boxes [k][m8][b4], one per MN atom
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (PF) ptx::tma_prefetch_4d(&tmA, c.ab, c.am + 8 * q, k0, c.ab2);
-            else ptx::tma_load_4d(st + q * (BK * 128), &tmA, bar, c.ab, c.am + 8 * q, k0, c.ab2);
+            if (PF) ptx::tma_prefetch_4d(tmA, c.ab, c.am + 8 * q, k0, c.ab2);
+            else ptx::tma_load_4d(st + q * (BK * 128), tmA, bar, c.ab, c.am + 8 * q, k0, c.ab2);
           }
         } else {
-          tma_operand<A_K, BK, PF>(&tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
+          tma_operand<BK, PF>(c.pr->a_k, tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
         }
-        tma_operand<B_K, BK, PF, HNT>(&tmB, st + Gm::A_BYTES, bar, c.bn, k0, c.bb, c.bb2, false,
-                                      false);
+        tma_operand<BK, PF, HNT>(c.pr->b_k, &c.pr->tb, st + Gm::A_BYTES, bar, c.bn, k0, c.bb,
+                                 c.bb2, false, false);
       };
       // L2 prefetch distance (K-blocks ahead of the smem ring)
       const int pfd = p_prefetch & 0xff;
       const bool dbg_no_tma = (p_prefetch >> 8) & 1;  // diagnostics: MMA/convert loop only
       int64_t pf_tile = pair;       // prefetch cursor (tile, k-block)
-      int pf_kb = 0;
-      Coord pf_c = decode(pf_tile);
+      int pf_kb = 0, pf_cur = 0, cur = 0;
+      Coord pf_c{};
+      if (pf_tile < total) pf_c = decode(pf_tile, pf_cur);
       auto prefetch_next = [&]() {
         if (pf_tile >= total) return;
         boxes(pf_c, pf_kb * BK, nullptr, nullptr, std::true_type{});
-        if (++pf_kb == nkb) {
+        if (++pf_kb == pf_c.pr->nkb) {
           pf_kb = 0;
           pf_tile += npairs;
-          if (pf_tile < total) pf_c = decode(pf_tile);
+          if (pf_tile < total) pf_c = decode(pf_tile, pf_cur);
         }
       };
       if (ptx::elect_one_sync())
@@ -301,7 +333,8 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       __syncwarp();
       int64_t g = 0;
       for (int64_t t = pair; t < total; t += npairs) {
-        const Coord c = decode(t);
+        const Coord c = decode(t, cur);
+        const int nkb = c.pr->nkb;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const uint32_t s = uint32_t(g % RAW_SLOTS);
           ptx::mbar_wait(&raw_empty[s], (uint32_t(g / RAW_SLOTS) & 1u) ^ 1u);
@@ -328,6 +361,11 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     uint32_t full_leader[RAW_SLOTS];
 #pragma unroll
     for (int s = 0; s < RAW_SLOTS; ++s) full_leader[s] = ptx::mapa(&full[s], 0);
+    int64_t n_iter = 0;  // K-blocks of this pair's tiles
+    {
+      int cur = 0;
+      for (int64_t t = pair; t < total; t += npairs) n_iter += locate(prs, nprob, t, cur).nkb;
+    }
     for (int64_t g = grp; g < n_iter; g += kConvWarps / kGroupWarps) {
       const uint32_t s = uint32_t(g % RAW_SLOTS);
       const uint32_t ls = uint32_t(g % LO_SLOTS);
@@ -371,15 +409,20 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
     // -------------------------------------------------------- epilogue
     const uint32_t lane_addr = uint32_t(warp * 32) << 16;
     const uint32_t empty_leader[2] = {ptx::mapa(&acc_empty[0], 0), ptx::mapa(&acc_empty[1], 0)};
+    const int r = warp * 32 + lane;
+    const bool leader = (r == 0);
+    uint32_t nchunk = 0, tcount = 0;
+    int cur = 0;
+    for (int64_t t = pair; t < total; t += npairs, ++tcount) {
+      const Problem& P = locate(prs, nprob, t, cur);
+      const GemmParams<float>& p = P.p;
+      const Fold& f = P.f;
+      const Tile tc = tile_of<BB, BNT>(t - P.tile_begin, P.tiles_m, P.tiles_n, P.nbatch);
     if (!BB && f.cmode) {
       // TMA-store epilogue: per 32-column chunk, TMEM -> registers (alpha) ->
       // smem staging (double-buffered) -> one TMA store of a 128 x 32 box.
       // The TMA engine writes full lines and clips the M / N tails.
-      const int r = warp * 32 + lane;
-      const bool leader = (r == 0);
-      uint32_t nchunk = 0, tcount = 0;
-      for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-        const Tile tc = tile_of<BB, BNT>(t, tiles_m, tiles_n, nbatch);
+      {
         const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
         const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
         ptx::mbar_wait(&acc_full[b], ph);
@@ -446,20 +489,17 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
               if (f.fn == 1) cb = y; else cb2 = y;
             }
             if (f.cmode == 1)
-              ptx::tma_store_4d(&tmC, epi_stage + buf * (128 * 32 * 4), int(row0), int(col0),
+              ptx::tma_store_4d(&P.tc, epi_stage + buf * (128 * 32 * 4), int(row0), int(col0),
                                 int(cb), int(cb2));
             else
-              ptx::tma_store_4d(&tmC, epi_stage + buf * (128 * 32 * 4), int(col0), int(row0),
+              ptx::tma_store_4d(&P.tc, epi_stage + buf * (128 * 32 * 4), int(col0), int(row0),
                                 int(cb), int(cb2));
             ptx::bulk_commit_group();
           }
         }
       }
-      if (leader) ptx::bulk_wait_group<0>();
     } else {
-    uint32_t tcount = 0;
-    for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-      const Tile tc = tile_of<BB, BNT>(t, tiles_m, tiles_n, nbatch);
+    {
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_full[b], ph);
@@ -467,7 +507,6 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
 #ifdef SBT_TRACE
       long long t_ld = 0, t_begin = clock64();
 #endif
-      const int r = warp * 32 + lane;
       // BB: MMA row r is (batch entry 4*pb + r%4, m = m0 + 32*rank + r/4);
       // fold: row r' = m0 + 128*rank + r of M' is (m = r' % m_in, x = r' / m_in)
       int64_t row = BB ? tc.m0 + rank * 32 + (r >> 2) : tc.m0 + rank * HM + r;
@@ -550,23 +589,30 @@ tf32x3_pair_tma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap 
       }
     }
     }  // direct-store epilogue
+    }  // tiles
+    if (leader) ptx::bulk_wait_group<0>();
   } else if (warp == 13 && rank == 0) {
     // -------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (waits and descriptor math are
     // warp-uniform); one elected lane issues the MMAs and commits.
-    constexpr uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);
+    // per-problem operand layouts (uniform registers)
     // K-major: rows of BK*4 bytes (SW128 for BK=32, SW64 for BK=16), 8-row
     // groups at SBO = 8*BK*4, K=8 step = 32 B inside the row.
     // MN-major: 32-wide MN slabs of BK k-rows: LBO = slab stride (BK*128 B),
     // SBO 512 (4-row K groups), K=8 step = 1024 B.
     constexpr uint32_t k_lay = BK == 32 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
-    constexpr uint32_t a_lbo = A_K ? 16u : uint32_t(BK * 128), a_sbo = A_K ? 8u * BK * 4 : 512u;
-    constexpr uint32_t b_lbo = B_K ? 16u : uint32_t(BK * 128), b_sbo = B_K ? 8u * BK * 4 : 512u;
-    constexpr uint32_t a_step = A_K ? 32u : 1024u, b_step = B_K ? 32u : 1024u;
-    constexpr uint32_t a_lay = A_K ? k_lay : ptx::kLayoutSW128Base32B;
-    constexpr uint32_t b_lay = B_K ? k_lay : ptx::kLayoutSW128Base32B;
     uint32_t it = 0, tcount = 0;
+    int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
+      const Problem& P = locate(prs, nprob, t, cur);
+      const bool A_K = !BB && P.a_k, B_K = P.b_k;
+      const int nkb = P.nkb;
+      const uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);
+      const uint32_t a_lbo = A_K ? 16u : uint32_t(BK * 128), a_sbo = A_K ? 8u * BK * 4 : 512u;
+      const uint32_t b_lbo = B_K ? 16u : uint32_t(BK * 128), b_sbo = B_K ? 8u * BK * 4 : 512u;
+      const uint32_t a_step = A_K ? 32u : 1024u, b_step = B_K ? 32u : 1024u;
+      const uint32_t a_lay = A_K ? k_lay : ptx::kLayoutSW128Base32B;
+      const uint32_t b_lay = B_K ? k_lay : ptx::kLayoutSW128Base32B;
       const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_empty[b], ph ^ 1u);

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/sbt200.h"
 #include "sbt_common.cuh"
@@ -85,6 +86,85 @@ static GemmParams<T> make(int64_t m, int64_t n, int64_t k, T alpha, const T* a, 
   p.alpha = alpha; p.beta = beta;
   if (oa < 0 || ob < 0 || oc < 0) { p.m = -1; }  // rejected by validate()
   return p;
+}
+
+template <typename T>
+static GemmParams<T> from_desc(const sbt_gemm_desc& d) {
+  return make<T>(d.m, d.n, d.k, T(d.alpha), static_cast<const T*>(d.a), d.oa, d.ars, d.acs,
+                 d.apt, d.apt2, static_cast<const T*>(d.b), d.ob, d.brs, d.bcs, d.bpt, d.bpt2,
+                 T(d.beta), static_cast<T*>(d.c), d.oc, d.crs, d.ccs, d.cpt, d.cpt2, d.batch,
+                 d.batch2);
+}
+
+// Grouped execution: see include/sbt200.h.  fp32 problems the pair kernel
+// takes are bucketed by kernel configuration and launched together.
+template <bool SPLIT, bool BB, int BNT>
+struct GroupRun {
+  static int run(const std::vector<PairPlan>& plans, const std::vector<int>& idx,
+                 cudaStream_t stream, std::vector<char>& launched) {
+    bool* flags = reinterpret_cast<bool*>(launched.data());
+    return GroupLaunch<SPLIT, BB, BNT>::run(plans.data(), idx.data(), int(idx.size()), stream,
+                                            flags);
+  }
+};
+
+template <typename T>
+static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream) {
+  if (count < 0 || (count > 0 && !descs)) return fail(SBT_EINVAL, "group: bad arguments");
+  std::vector<GemmParams<T>> ps;
+  ps.reserve(count);
+  for (int i = 0; i < count; ++i) {
+    GemmParams<T> p = from_desc<T>(descs[i]);
+    const int rc = validate(p);
+    if (rc != SBT_OK) return rc;
+    ps.push_back(p);
+  }
+  std::vector<char> launched(count, 0);
+  if constexpr (sizeof(T) == 4) {
+    if (kernel_override() == 0) {
+      // bucket the pair-kernel problems by configuration (bb, split, bnt)
+      std::vector<PairPlan> plans(count);
+      std::vector<int> buckets[10];
+      for (int i = 0; i < count; ++i) {
+        const GemmParams<float>& p = ps[i];
+        if (p.batch == 0 || p.batch2 == 0) { launched[i] = 1; continue; }
+        if (p.k > kMaxChunkK) continue;                       // K-chunked: single path
+        if (!plan_pair(p, &plans[i])) continue;
+        const PairPlan& pl = plans[i];
+        const int key = pl.bb ? (pl.split ? 9 : 8)
+                              : ((pl.bnt == 32 ? 0 : pl.bnt == 64 ? 1 : pl.bnt == 128 ? 2 : 3) * 2 +
+                                 (pl.split ? 1 : 0));
+        buckets[key].push_back(i);
+      }
+      for (int key = 0; key < 10; ++key) {
+        if (buckets[key].empty()) continue;
+        const PairPlan& pl0 = plans[buckets[key][0]];
+        int rc;
+        if (pl0.bb) {
+          rc = pl0.split ? GroupRun<true, true, 256>::run(plans, buckets[key], stream, launched)
+                         : GroupRun<false, true, 256>::run(plans, buckets[key], stream, launched);
+        } else {
+          switch (pl0.bnt) {
+            case 32: rc = pl0.split ? GroupRun<true, false, 32>::run(plans, buckets[key], stream, launched)
+                                    : GroupRun<false, false, 32>::run(plans, buckets[key], stream, launched); break;
+            case 64: rc = pl0.split ? GroupRun<true, false, 64>::run(plans, buckets[key], stream, launched)
+                                    : GroupRun<false, false, 64>::run(plans, buckets[key], stream, launched); break;
+            case 128: rc = pl0.split ? GroupRun<true, false, 128>::run(plans, buckets[key], stream, launched)
+                                     : GroupRun<false, false, 128>::run(plans, buckets[key], stream, launched); break;
+            default: rc = pl0.split ? GroupRun<true, false, 256>::run(plans, buckets[key], stream, launched)
+                                    : GroupRun<false, false, 256>::run(plans, buckets[key], stream, launched); break;
+          }
+        }
+        if (rc < 0) return rc;
+      }
+    }
+  }
+  for (int i = 0; i < count; ++i) {  // everything not grouped: one call each
+    if (launched[i]) continue;
+    const int rc = run<T>(ps[i], stream);
+    if (rc != SBT_OK) return rc;
+  }
+  return check_cuda(cudaGetLastError(), "group launch");
 }
 
 // ---- host-buffer path -------------------------------------------------------
@@ -298,6 +378,13 @@ int sbt_probe_tf32_sustained(double seconds, double* tflops) {
   cudaEventDestroy(e1);
   note_launch("probe_tf32_umma");
   return check_cuda(cudaGetLastError(), "probe");
+}
+
+int sbt_batched_core_group_f32(int count, const sbt_gemm_desc* descs, void* stream) {
+  return sbt::run_group<float>(count, descs, (cudaStream_t)stream);
+}
+int sbt_batched_core_group_f64(int count, const sbt_gemm_desc* descs, void* stream) {
+  return sbt::run_group<double>(count, descs, (cudaStream_t)stream);
 }
 
 int sbt_permute_f64(int order, const int64_t* dims, const double* src, const int64_t* src_strides,

@@ -137,13 +137,131 @@ static tf32tma::Fold make_fold(const GemmParams<float>& p) {
   return f;
 }
 
-template <bool AK, bool BK_, bool SPLIT, int KB, bool BB = false, int BNT = 256>
-static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
-                             tf32tma::Fold f = tf32tma::Fold{0, 0, 0, 0, 0, 0, 0}) {
-  if (f.mtot == 0) f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0, 0};
-  auto kern = tf32tma::tf32x3_pair_tma_kernel<AK, BK_, SPLIT, KB, BB, BNT>;
-  constexpr int smem = tf32tma::Geo<KB, BB, BNT>::SMEM_BYTES;
+// ---- CTA-pair tcgen05 kernel: planning, problem sets, launches --------------
+
+// How one GEMM request maps onto the pair kernel (orientation, layouts, fold,
+// tile width, accumulator split).
+struct PairPlan {
+  GemmParams<float> p;  // oriented problem
+  tf32tma::Fold f;
+  int am = 0, bm = 0;   // 1 = K-major, 2 = MN-major
+  bool bb = false, split = false;
+  int bnt = 256;
+};
+
+static bool pick_split(const GemmParams<float>& p) {
+  static const int split_env = env_int("SBT_TC_SPLITACC", -1);
+  return split_env < 0 ? (p.k > 512) : (split_env != 0);
+}
+
+// Decide whether (and how) the pair kernel runs this request.
+// variant (SBT_TC_VARIANT): 0 auto, 1 = 1-CTA tiles only, 4 = force pair,
+// 5 = batch-blocked pair only, 6 = auto without batch folding
+static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
+  static const int variant = env_int("SBT_TC_VARIANT", 0);
+  if (variant == 1) return false;
+  if (variant == 0 || variant == 5) {
+    // exceptional cases: A unit-stride along the batch, B batch-independent
+    for (int o = 0; o < 2; ++o) {
+      const GemmParams<float> p = o ? transposed(p0) : p0;
+      if (p.aps != 1 || p.bps != 0 || p.batch < 2 || !aligned16(p.a)) continue;
+      if (p.ars < 4 || p.acs < 4 || !vmult<float>(p.ars) || !vmult<float>(p.acs) ||
+          !vmult<float>(p.aps2))
+        continue;
+      if (p.m < 64 || p.n < 192) continue;
+      const int bm = b_major(p);
+      if (!bm) continue;
+      out->p = p;
+      out->f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0, 0};
+      out->am = 2; out->bm = bm; out->bb = true; out->bnt = 256; out->split = pick_split(p);
+      return true;
+    }
+    if (variant == 5) return false;
+  }
+  // among the two orientations (C = AB, C^T = B^T A^T) take the one whose
+  // (folded) M reaches a full 256-row tile, larger M first
+  bool found = false;
+  for (int o = 0; o < 2; ++o) {
+    const GemmParams<float> q = o ? transposed(p0) : p0;
+    const int qa = a_major(q), qb = b_major(q);
+    if (!qa || !qb) continue;
+    const tf32tma::Fold f =
+        variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q);
+    // narrow N (< 96) only pays off for many M rows in total (HBM-bound skinny
+    // products: rank-r Tucker mode products); narrow tiles need K-major B
+    const int64_t rows = f.mtot * ((f.fm == 1 || f.fn == 1) ? 1 : q.batch) *
+                         ((f.fm == 2 || f.fn == 2) ? 1 : q.batch2);
+    const bool ok = variant == 4 ||
+                    (f.mtot >= 256 && (f.ntot >= 96 || (f.ntot >= 16 && rows >= 8192 && qb == 1)));
+    if (ok && (!found || f.mtot > out->f.mtot ||
+               (f.mtot == out->f.mtot && f.ntot > out->f.ntot))) {
+      out->p = q; out->f = f; out->am = qa; out->bm = qb; found = true;
+    }
+  }
+  if (!found) return false;
+  const int64_t nt = out->f.ntot;
+  out->bnt = nt <= 32 ? 32 : nt <= 64 ? 64 : nt < 192 ? 128 : 256;
+  if (out->bnt < 64 && out->bm != 1) return false;  // 16-column B halves must be K-major
+  out->bb = false;
+  out->split = pick_split(out->p);
+  return true;
+}
+
+// Tensor maps, tile grid and epilogue mode of one planned problem.
+template <bool BB, int BNT, int KB>
+static bool fill_problem(const PairPlan& pl, tf32tma::Problem* pr) {
+  const GemmParams<float>& p = pl.p;
+  tf32tma::Fold f = pl.f;
   constexpr uint32_t HNT = BNT / 2;
+  const bool AK = pl.am == 1, BK_ = pl.bm == 1;
+  const CUtensorMapSwizzle kswz = KB == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const bool ok_a =
+      BB ? make_tmap_f32(&pr->ta, p.a, p.batch, p.m, p.ars, p.k, p.acs, p.batch2, p.aps2, 4, 8,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, KB)
+      : AK ? make_tmap_f32(&pr->ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, KB,
+                           128, kswz)
+           : make_tmap_f32(&pr->ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32,
+                           KB, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const bool ok_b =
+      BK_ ? make_tmap_f32(&pr->tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB,
+                          HNT, kswz)
+          : make_tmap_f32(&pr->tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32,
+                          KB, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!ok_a || !ok_b) return false;  // not expressible as TMA: caller falls back
+  // TMA-store epilogue when C is expressible as a tensor map (beta == 0: C not read)
+  std::memset(&pr->tc, 0, sizeof(pr->tc));
+  f.cmode = 0;
+  static const int tma_epi = env_int("SBT_TC_TMA_EPI", 1);
+  if (!BB && tma_epi && p.beta == 0.f && aligned16(p.c) && vmult<float>(p.cps) &&
+      vmult<float>(p.cps2)) {
+    if (p.crs == 1 && vmult<float>(p.ccs) &&
+        make_tmap_f32(&pr->tc, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 128, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE))
+      f.cmode = 1;
+    else if (p.ccs == 1 && vmult<float>(p.crs) &&
+             make_tmap_f32(&pr->tc, p.c, p.n, p.m, p.crs, p.batch, p.cps, p.batch2, p.cps2, 32,
+                           128, CU_TENSOR_MAP_SWIZZLE_128B))
+      f.cmode = 2;
+  }
+  pr->p = p;
+  pr->f = f;
+  pr->tiles_m = ceil_div(f.mtot, BB ? 64 : tf32tma::BM);
+  pr->tiles_n = ceil_div(f.ntot, BNT);
+  pr->nbatch = BB ? ceil_div(p.batch, 4) : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
+  pr->a_k = AK ? 1 : 0;
+  pr->b_k = BK_ ? 1 : 0;
+  pr->nkb = int(ceil_div(p.k, KB));
+  pr->pad = 0;
+  return true;
+}
+
+// Launch one problem set (tile_begin of each problem must be set, total summed).
+template <int MAXP, bool SPLIT, bool BB, int BNT, int KB = 32>
+static int launch_pair_set(const tf32tma::ProblemSet<MAXP>& ps, cudaStream_t stream,
+                           const char* name) {
+  static_assert(sizeof(tf32tma::ProblemSet<MAXP>) <= 32000, "kernel parameter space");
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<MAXP, SPLIT, KB, BB, BNT>;
+  constexpr int smem = tf32tma::Geo<KB, BB, BNT>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -151,109 +269,98 @@ static int launch_tf32tma_kb(const GemmParams<float>& p, cudaStream_t stream,
       return -3;
     attr_set = true;
   }
-  const CUtensorMapSwizzle kswz = KB == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  CUtensorMap ta, tb;
-  const bool ok_a =
-      BB ? make_tmap_f32(&ta, p.a, p.batch, p.m, p.ars, p.k, p.acs, p.batch2, p.aps2, 4, 8,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, KB)
-      : AK ? make_tmap_f32(&ta, p.a, p.k, p.m, p.ars, p.batch, p.aps, p.batch2, p.aps2, KB, 128,
-                           kswz)
-           : make_tmap_f32(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, p.batch2, p.aps2, 32, KB,
-                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  const bool ok_b =
-      BK_ ? make_tmap_f32(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, p.batch2, p.bps2, KB, HNT,
-                          kswz)
-          : make_tmap_f32(&tb, p.b, p.n, p.k, p.brs, p.batch, p.bps, p.batch2, p.bps2, 32, KB,
-                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  if (!ok_a || !ok_b) return 0;  // not expressible as TMA: caller falls back
-  // TMA-store epilogue when C is expressible as a tensor map (beta == 0: C not read)
-  CUtensorMap tcm;
-  std::memset(&tcm, 0, sizeof(tcm));
-  f.cmode = 0;
-  static const int tma_epi = env_int("SBT_TC_TMA_EPI", 1);
-  if (!BB && tma_epi && p.beta == 0.f && aligned16(p.c) && vmult<float>(p.cps) &&
-      vmult<float>(p.cps2)) {
-    if (p.crs == 1 && vmult<float>(p.ccs) &&
-        make_tmap_f32(&tcm, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 128, 32,
-                      CU_TENSOR_MAP_SWIZZLE_NONE))
-      f.cmode = 1;
-    else if (p.ccs == 1 && vmult<float>(p.crs) &&
-             make_tmap_f32(&tcm, p.c, p.n, p.m, p.crs, p.batch, p.cps, p.batch2, p.cps2, 32, 128,
-                           CU_TENSOR_MAP_SWIZZLE_128B))
-      f.cmode = 2;
-  }
-  const int64_t tiles_m = ceil_div(f.mtot, BB ? 64 : tf32tma::BM);
-  const int64_t tiles_n = ceil_div(f.ntot, BNT);
-  const int64_t nb = BB ? ceil_div(p.batch, 4) : ((f.fm == 1 || f.fn == 1) ? 1 : p.batch);
-  const int64_t nb2 = (f.fm == 2 || f.fn == 2) ? 1 : p.batch2;
-  const int64_t total = tiles_m * tiles_n * nb * nb2;
-  const int64_t pairs = total < kNumSMs / 2 ? total : kNumSMs / 2;
+  const int64_t pairs = ps.total < kNumSMs / 2 ? ps.total : kNumSMs / 2;
   // low byte: L2 prefetch distance (measured: no gain, 0); bits 8/9: diagnostics
   // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
   static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8);
-  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(
-      p, ta, tb, tcm, tiles_m, tiles_n, total, f, prefetch);
-  note_launch(BB ? (SPLIT ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb")
-                 : (f.fm || f.fn)
-                     ? (BNT < 256 ? (SPLIT ? "tc_tf32x3_pair_fold_narrow_splitacc"
-                                           : "tc_tf32x3_pair_fold_narrow")
-                                  : (SPLIT ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold"))
-                     : (BNT < 256 ? (SPLIT ? "tc_tf32x3_pair_narrow_splitacc" : "tc_tf32x3_pair_narrow")
-                                  : (SPLIT ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma")));
+  kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(ps, prefetch);
+  note_launch(name);
   return 1;
 }
 
-// Batch-blocked pair kernel for the exceptional cases: A unit-stride along
-// the batch, B batch-independent (see k_tf32x3_pair_tma.cuh).  Tries the
-// problem as given and transposed; returns 1 if launched, 0 if not eligible.
-template <bool SPLIT>
-static int launch_tf32_bb(const GemmParams<float>& p0, cudaStream_t stream) {
-  static const int kb = env_int("SBT_TC_BK", 32);
-  for (int orient = 0; orient < 2; ++orient) {
-    const GemmParams<float> p = orient ? transposed(p0) : p0;
-    if (p.aps != 1 || p.bps != 0 || p.batch < 2 || !aligned16(p.a)) continue;
-    if (p.ars < 4 || p.acs < 4 || !vmult<float>(p.ars) || !vmult<float>(p.acs) ||
-        !vmult<float>(p.aps2))
-      continue;
-    if (p.m < 64 || p.n < 192) continue;
-    const int bm = b_major(p);
-    if (!bm) continue;
-    (void)kb;  // BK = 32 only (the BK = 16 variant measured slower)
-    if (bm == 1) return launch_tf32tma_kb<false, true, SPLIT, 32, true>(p, stream);
-    return launch_tf32tma_kb<false, false, SPLIT, 32, true>(p, stream);
+static const char* pair_name(bool bb, bool split, int bnt, bool fold, bool group) {
+  if (group) return bb ? "tc_tf32x3_pair_group_bb" : "tc_tf32x3_pair_group";
+  if (bb) return split ? "tc_tf32x3_pair_bb_splitacc" : "tc_tf32x3_pair_bb";
+  if (fold) {
+    if (bnt < 256) return split ? "tc_tf32x3_pair_fold_narrow_splitacc" : "tc_tf32x3_pair_fold_narrow";
+    return split ? "tc_tf32x3_pair_fold_splitacc" : "tc_tf32x3_pair_fold";
   }
-  return 0;
+  if (bnt < 256) return split ? "tc_tf32x3_pair_narrow_splitacc" : "tc_tf32x3_pair_narrow";
+  return split ? "tc_tf32x3_pair_tma_splitacc" : "tc_tf32x3_pair_tma";
 }
 
-template <bool AK, bool BK_, bool SPLIT, int BNT>
-static int launch_tf32tma_cfg(const GemmParams<float>& p, cudaStream_t stream,
-                              const tf32tma::Fold& f) {
-  return launch_tf32tma_kb<AK, BK_, SPLIT, 32, false, BNT>(p, stream, f);
+template <bool SPLIT, bool BB, int BNT>
+static int launch_pair_single_t(const PairPlan& pl, cudaStream_t stream) {
+  tf32tma::ProblemSet<1> ps;
+  if (!fill_problem<BB, BNT, 32>(pl, &ps.pr[0])) return 0;
+  ps.pr[0].tile_begin = 0;
+  ps.n = 1;
+  ps.total = ps.pr[0].tiles_m * ps.pr[0].tiles_n * ps.pr[0].nbatch *
+             ((ps.pr[0].f.fm == 2 || ps.pr[0].f.fn == 2) ? 1 : pl.p.batch2);
+  return launch_pair_set<1, SPLIT, BB, BNT>(
+      ps, stream, pair_name(BB, SPLIT, BNT, pl.f.fm || pl.f.fn, false));
 }
 
-template <bool SPLIT, int BNT>
-static int launch_tf32tma(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
-                          const tf32tma::Fold& f) {
-  if constexpr (BNT < 64) {  // narrow tiles: B must be K-major (16-column halves)
-    if (bm != 1) return 0;
-    return am == 1 ? launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f)
-                   : launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
-  } else {
-    if (am == 1 && bm == 1) return launch_tf32tma_cfg<true, true, SPLIT, BNT>(p, s, f);
-    if (am == 1) return launch_tf32tma_cfg<true, false, SPLIT, BNT>(p, s, f);
-    if (bm == 1) return launch_tf32tma_cfg<false, true, SPLIT, BNT>(p, s, f);
-    return launch_tf32tma_cfg<false, false, SPLIT, BNT>(p, s, f);
+// dispatch on the compile-time configuration of a plan
+template <template <bool, bool, int> class F, typename... Args>
+static int with_pair_cfg(const PairPlan& pl, Args&&... args) {
+  if (pl.bb) return pl.split ? F<true, true, 256>::run(args...) : F<false, true, 256>::run(args...);
+  switch (pl.bnt) {
+    case 32: return pl.split ? F<true, false, 32>::run(args...) : F<false, false, 32>::run(args...);
+    case 64: return pl.split ? F<true, false, 64>::run(args...) : F<false, false, 64>::run(args...);
+    case 128:
+      return pl.split ? F<true, false, 128>::run(args...) : F<false, false, 128>::run(args...);
+    default:
+      return pl.split ? F<true, false, 256>::run(args...) : F<false, false, 256>::run(args...);
   }
 }
 
-template <bool SPLIT>
-static int launch_tf32tma_w(const GemmParams<float>& p, int am, int bm, cudaStream_t s,
-                            const tf32tma::Fold& f) {
-  if (f.ntot <= 32) return launch_tf32tma<SPLIT, 32>(p, am, bm, s, f);
-  if (f.ntot <= 64) return launch_tf32tma<SPLIT, 64>(p, am, bm, s, f);
-  if (f.ntot < 192) return launch_tf32tma<SPLIT, 128>(p, am, bm, s, f);
-  return launch_tf32tma<SPLIT, 256>(p, am, bm, s, f);
+template <bool SPLIT, bool BB, int BNT>
+struct SingleLaunch {
+  static int run(const PairPlan& pl, cudaStream_t stream) {
+    return launch_pair_single_t<SPLIT, BB, BNT>(pl, stream);
+  }
+};
+
+static int try_pair_f32(const GemmParams<float>& p0, cudaStream_t stream) {
+  PairPlan pl;
+  if (!plan_pair(p0, &pl)) return 0;
+  return with_pair_cfg<SingleLaunch>(pl, pl, stream);
 }
+
+// ---- grouped launch: many independent problems, one persistent pair kernel --
+constexpr int kMaxGroup = 40;
+
+template <bool SPLIT, bool BB, int BNT>
+struct GroupLaunch {
+  // plans[idx[0..count)] share this configuration
+  static int run(const PairPlan* plans, const int* idx, int count, cudaStream_t stream,
+                 bool* launched) {
+    thread_local tf32tma::ProblemSet<kMaxGroup> ps;  // host staging (the launch copies it)
+    int rc = 0;
+    for (int base = 0; base < count && rc >= 0; base += kMaxGroup) {
+      const int nb = (count - base) < kMaxGroup ? (count - base) : kMaxGroup;
+      int n = 0;
+      int64_t total = 0;
+      int members[kMaxGroup];
+      for (int i = 0; i < nb; ++i) {
+        const PairPlan& pl = plans[idx[base + i]];
+        if (!fill_problem<BB, BNT, 32>(pl, &ps.pr[n])) continue;  // caller relaunches singly
+        ps.pr[n].tile_begin = total;
+        total += ps.pr[n].tiles_m * ps.pr[n].tiles_n * ps.pr[n].nbatch *
+                 ((ps.pr[n].f.fm == 2 || ps.pr[n].f.fn == 2) ? 1 : pl.p.batch2);
+        members[n++] = idx[base + i];
+      }
+      if (n == 0) continue;
+      ps.n = n;
+      ps.total = total;
+      rc = launch_pair_set<kMaxGroup, SPLIT, BB, BNT>(ps, stream, pair_name(BB, SPLIT, BNT, false, true));
+      if (rc >= 0)
+        for (int i = 0; i < n; ++i) launched[members[i]] = true;
+    }
+    return rc;
+  }
+};
 
 template <int BN>
 static int launch_tf32x3_bn(const GemmParams<float>& p, int am, int bm, cudaStream_t s) {
@@ -362,45 +469,9 @@ static int try_tensor_f64(const GemmParams<double>& p0, cudaStream_t stream, boo
 
 // Returns 1 if launched, 0 if not eligible, <0 on error.
 static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool forced) {
-  static const int variant = env_int("SBT_TC_VARIANT", 0);
-  if (variant == 0 || variant == 5) {
-    static const int split_env = env_int("SBT_TC_SPLITACC", -1);
-    const bool split = split_env < 0 ? (p0.k > 512) : (split_env != 0);
-    const int rc = split ? launch_tf32_bb<true>(p0, stream) : launch_tf32_bb<false>(p0, stream);
+  {
+    const int rc = try_pair_f32(p0, stream);
     if (rc != 0) return rc;
-  }
-  // 0 auto, 1 = 1-CTA tiles only, 4 = CTA-pair TMA kernel, 5 = batch-blocked pair,
-  // 6 = auto without batch folding
-  if (variant == 0 || variant == 4 || variant == 6) {
-    // CTA-pair kernel: among the two orientations (C = AB, C^T = B^T A^T) take
-    // the one whose (folded) M reaches a full 256-row tile, larger M first;
-    // tile width 256, or 128 when N' < 192
-    GemmParams<float> best{};
-    tf32tma::Fold bf{};
-    int ba = 0, bb = 0;
-    bool found = false;
-    for (int o = 0; o < 2; ++o) {
-      const GemmParams<float> q = o ? transposed(p0) : p0;
-      const int qa = a_major(q), qb = b_major(q);
-      if (!qa || !qb) continue;
-      const tf32tma::Fold f = variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q);
-      // narrow N (< 96) only pays off for many M rows in total (HBM-bound
-      // skinny products: rank-r Tucker mode products)
-      const int64_t rows = f.mtot * ((f.fm == 1 || f.fn == 1) ? 1 : q.batch) *
-                           ((f.fm == 2 || f.fn == 2) ? 1 : q.batch2);
-      const bool ok = variant == 4 ||
-                      (f.mtot >= 256 && (f.ntot >= 96 || (f.ntot >= 16 && rows >= 8192 && qb == 1)));
-      if (ok && (!found || f.mtot > bf.mtot || (f.mtot == bf.mtot && f.ntot > bf.ntot))) {
-        best = q; bf = f; ba = qa; bb = qb; found = true;
-      }
-    }
-    if (found) {
-      static const int split_env = env_int("SBT_TC_SPLITACC", -1);
-      const bool split = split_env < 0 ? (best.k > 512) : (split_env != 0);
-      const int rc = split ? launch_tf32tma_w<true>(best, ba, bb, stream, bf)
-                           : launch_tf32tma_w<false>(best, ba, bb, stream, bf);
-      if (rc != 0) return rc;
-    }
   }
   GemmParams<float> p;
   int am = 0, bm = 0;

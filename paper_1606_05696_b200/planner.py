@@ -631,6 +631,68 @@ def execute_plan(plan: EvaluationPlan, a: DenseTensor, b: DenseTensor,
             counters.kernel_calls[L.kind] = counters.kernel_calls.get(L.kind, 0) + 1
 
 
+def execute_plans(calls) -> None:
+    """Run several INDEPENDENT planned contractions as one grouped call of the
+    library (``sbt_batched_core_group_*``): the ones the CTA-pair tensor-core
+    kernel takes share one persistent launch per kernel configuration, so a
+    batch of contractions pays one pipeline fill / drain / tile tail instead of
+    one per contraction.  ``calls`` is a sequence of
+    (plan, a, b, alpha, beta, c) with the arguments of execute_plan.  No call's
+    C may overlap another call's A, B or C (ValueError otherwise).  Single-mode
+    plans only; results equal running execute_plan on each call."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    calls = list(calls)
+    if not calls:
+        return
+    descs = []
+    dtype = None
+    device = None
+    spans = []
+    for plan, a, b, alpha, beta, c in calls:
+        _check_tensor(plan.layout_a, a, "A")
+        _check_tensor(plan.layout_b, b, "B")
+        _check_tensor(plan.layout_c, c, "C")
+        if _storage_overlap(c.data, a.data) or _storage_overlap(c.data, b.data):
+            raise PlanError("C must not alias A or B")
+        if plan.strategy not in ("flattened-gemm", "strided-batched", "nested-batched",
+                                 "extended-batched"):
+            raise PlanError(f"strategy {plan.strategy!r} cannot be grouped")
+        if dtype is None:
+            dtype, device = c.data.dtype, c.data.device
+        if a.data.dtype != dtype or b.data.dtype != dtype or c.data.dtype != dtype:
+            raise ValueError("grouped calls must share one dtype")
+        if c.data.device != device or a.data.device != device or b.data.device != device:
+            raise ValueError("grouped calls must share one device")
+        L = lower_plan(plan)
+        x, y = (a.data, b.data) if L.first == "A" else (b.data, a.data)
+        ars, acs, apt, apt2, brs, bcs, bpt, bpt2, crs, ccs, cpt, cpt2 = L.strides
+        for ox, oy, oc in L.outer:
+            descs.append(_lib.GemmDesc(L.m, L.n, L.k, float(alpha), float(beta),
+                                       x.data_ptr(), ox, ars, acs, apt, apt2,
+                                       y.data_ptr(), oy, brs, bcs, bpt, bpt2,
+                                       c.data.data_ptr(), oc, crs, ccs, cpt, cpt2,
+                                       L.batch, L.batch2))
+        spans.append((c.data, a.data, b.data))
+    for i, (ci, _, _) in enumerate(spans):
+        for j, (cj, aj, bj) in enumerate(spans):
+            if i != j and (_storage_overlap(ci, cj) or _storage_overlap(ci, aj) or
+                           _storage_overlap(ci, bj)):
+                raise ValueError(f"grouped calls {i} and {j} are not independent "
+                                 "(a C overlaps another call's operands)")
+    arr = (_lib.GemmDesc * len(descs))(*descs)
+    lib = _lib.load()
+    fn = lib.sbt_batched_core_group_f64 if dtype == torch.float64 else \
+        lib.sbt_batched_core_group_f32
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device).cuda_stream
+        _lib.check(fn(len(descs), ctypes.cast(arr, ctypes.POINTER(_lib.GemmDesc)), stream),
+                   "grouped strided batched GEMM")
+
+
 # ---------------------------------------------------------------------------
 # reporting
 

@@ -699,3 +699,59 @@ def test_narrow_tiles_for_skinny_products(m, n, k, P):
     want = A @ B
     got = host(c).reshape(P, n, m).transpose(0, 2, 1)
     assert naive.max_rel_err(got, want) <= TOL[torch.float32]
+
+
+# ------------------------------------------------------------------ grouped execution
+
+
+@pytest.mark.parametrize("n,dtype", [(64, torch.float32), (128, torch.float32),
+                                     (256, torch.float32), (64, torch.float64)])
+def test_grouped_execution_equals_single_calls(n, dtype):
+    """execute_plans (one persistent launch per kernel configuration) gives
+    bitwise the results of per-call execute_plan for all 36 cases, with
+    distinct outputs, and matches the oracle."""
+    rng = np.random.default_rng(n)
+    calls, singles = [], []
+    for i, case in enumerate(enumerate_cases(2, 3)):
+        spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+        la, lb, lc = _packed(spec, dict(m=n, n=n, p=n, k=n))
+        a = DenseTensor(la, dev(rng.uniform(-1, 1, la.size), dtype))
+        b = DenseTensor(lb, dev(rng.uniform(-1, 1, lb.size), dtype))
+        c0 = rng.uniform(-1, 1, lc.size)
+        beta = 0.5 if i % 5 == 0 else 0.0
+        plan = plan_single_mode(spec, la, lb, lc)
+        cg = DenseTensor(lc, dev(c0, dtype))
+        cs = DenseTensor(lc, dev(c0, dtype))
+        calls.append((plan, a, b, 1.25, beta, cg))
+        singles.append((plan, a, b, 1.25, beta, cs))
+    n0 = _lib.launch_count()
+    sbt.execute_plans(calls)
+    torch.cuda.synchronize()
+    grouped_launches = _lib.launch_count() - n0
+    for plan, a, b, al, be, cs in singles:
+        execute_plan(plan, a, b, al, be, cs)
+    torch.cuda.synchronize()
+    if dtype == torch.float32 and n >= 128:
+        assert grouped_launches < 36, grouped_launches
+    for (plan, a, b, al, be, cg), (_, _, _, _, _, cs) in zip(calls, singles):
+        assert torch.equal(cg.data, cs.data), plan.spec
+    # and one of them (beta = 0) against the oracle
+    plan, a, b, al, be, cg = calls[-2]
+    assert be == 0.0
+    spec = plan.spec
+    ext = dict(m=n, n=n, p=n, k=n)
+    want = np.zeros(plan.layout_c.size)
+    oplan.contract(spec.labels_a, spec.labels_b, spec.labels_c, ext, host(a.data),
+                   host(b.data), al, 0.0, want)
+    assert naive.max_rel_err(host(cg.data), want) <= TOL[dtype]
+
+
+def test_grouped_execution_rejects_dependent_calls():
+    spec = ContractionSpec(tuple("mk"), tuple("knp"), tuple("mnp"))
+    la, lb, lc = Layout.packed((8, 4)), Layout.packed((4, 8, 8)), Layout.packed((8, 8, 8))
+    a = DenseTensor(la, dev(np.ones(la.size)))
+    b = DenseTensor(lb, dev(np.ones(lb.size)))
+    c = DenseTensor(lc, dev(np.zeros(lc.size)))
+    plan = plan_single_mode(spec, la, lb, lc)
+    with pytest.raises(ValueError):
+        sbt.execute_plans([(plan, a, b, 1.0, 0.0, c), (plan, a, b, 1.0, 0.0, c)])

@@ -27,10 +27,10 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(tr.data(), tf32tma::g_trace, tr.size() * 8);
   const char* names[4] = {"tma_slot_free", "conv_raw_landed", "conv_done", "mma_full"};
   for (int rk = 0; rk < 2; ++rk)
-    for (int row = 0; row < 4; ++row) {
+    for (int row = (rk ? 3 : 0); row < 4; ++row) {
       printf("rank%d %-16s", rk, names[row]);
       long long t0 = tr[(0) * 4096];
-      for (int g = 0; g < 40; ++g) printf(" %lld", tr[(row + 4 * rk) * 4096 + g] ? (tr[(row + 4 * rk) * 4096 + g] - t0) : -1);
+      for (int g = 40; g < 72; ++g) printf(" %lld", tr[(row + 4 * rk) * 4096 + g] ? (tr[(row + 4 * rk) * 4096 + g] - t0) : -1);
       printf("\n");
     }
   long long ep[2][64][4];

@@ -33,6 +33,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "contraction GFLOP/s and % roofline vs n (1/2/4/8 B200) next to CPU ref"
+EXCEPTIONAL_CASES = {"3.4", "3.6", "4.4", "4.6", "5.4", "5.6", "6.4", "6.6"}
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
 FP64_NOMINAL_TFLOPS = 37.0  # HGX B200 datasheet FP64 / FP64 tensor core
 
@@ -122,7 +123,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- GPU arm
 
 
-def build_sets(cases, n, dtype, device, nsets, seed):
+def build_sets(cases, n, dtype, device, nsets, seed, distinct_c=False):
     import torch
     from paper_1606_05696_b200.layout import DenseTensor, Layout
     from paper_1606_05696_b200.planner import plan_single_mode
@@ -143,6 +144,8 @@ def build_sets(cases, n, dtype, device, nsets, seed):
         from paper_1606_05696_b200.notation import ContractionSpec
         plan = plan_single_mode(ContractionSpec(*spec_labels), la, lb, lc)
         a, b, c = sets[i % nsets]
+        if distinct_c:  # grouped execution: every case writes its own C
+            c = torch.empty(size_b, device=device, dtype=dtype)
         # the order-2 operand may be A or B of the case: bind buffers by size
         ta = DenseTensor(la, a if la.size == size_a else b)
         tb = DenseTensor(lb, a if lb.size == size_a else b)
@@ -192,7 +195,15 @@ def run_gpu(args):
     # 4 rotating operand sets: with the step's cases issued round-robin on 2
     # streams, cases that can run concurrently never share a buffer (cases
     # sharing a set share a stream and are ordered)
-    work = build_sets(cases, n, dtype, device, 4, seed=1234 + rank)
+    # grouped mode: the step's independent contractions go through ONE
+    # execute_plans call (one persistent launch per kernel configuration);
+    # every case then needs its own C (36 x n^3 elements)
+    # (n >= 512: one case is >= 0.5 ms, launch overheads are negligible and
+    # separate launches on two streams fill each other's tails better)
+    group = (not args.no_group) and n <= 256
+    work = build_sets(cases, n, dtype, device, 4, seed=1234 + rank, distinct_c=group)
+    from paper_1606_05696_b200.planner import execute_plans
+    exceptional = {cid for cid, *_ in work if cid in EXCEPTIONAL_CASES}
     stream = torch.cuda.current_stream(device)
 
     def barrier():
@@ -220,6 +231,40 @@ def run_gpu(args):
     per_case = [[ev[st][i].elapsed_time(ev[st][i + 1]) for st in range(args.steps)]
                 for i in range(nc)]
     nograph_ms = ev[0][0].elapsed_time(ev[-1][nc]) / args.steps
+    group_attr = None
+    if group:
+        # one grouped launch per subset (plain cases / exceptional cases), each
+        # captured in a CUDA graph and timed with events on the launching stream
+        subsets = {"tc_tf32x3_pair_group" if dtype == torch.float32 else "grouped_f64":
+                   [w for w in work if w[0] not in exceptional],
+                   "tc_tf32x3_pair_group_bb" if dtype == torch.float32 else "grouped_f64_bb":
+                   [w for w in work if w[0] in exceptional]}
+        group_attr = {}
+        for name, sub in subsets.items():
+            if not sub:
+                continue
+            calls = [(plan, a, b, 1.0, 0.0, c) for cid, plan, a, b, c in sub]
+            for _ in range(2):
+                execute_plans(calls)
+            sub_graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(device)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(sub_graph, stream=cap):
+                    execute_plans(calls)
+            stream.wait_stream(cap)
+            sub_graph.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                sub_graph.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            group_attr[name] = {"cases": len(sub), "ms": round(ms, 4),
+                                "launch_kernel": _lib.last_kernel(),
+                                "tflops": round(len(sub) * 2.0 * n ** 4 / (ms * 1e-3) / 1e12, 2)}
 
     # (2) the timed steps: the step's 36 independent contractions issued
     # round-robin on args.streams CUDA streams (one library launch each, so a
@@ -228,6 +273,21 @@ def run_gpu(args):
     side = [torch.cuda.Stream(device) for _ in range(max(0, args.streams - 1))]
 
     def issue_step(main):
+        if group:
+            # plain and exceptional cases as two grouped calls on two streams
+            # (their persistent launches overlap each other's tails)
+            subs = [[w for w in work if w[0] not in exceptional],
+                    [w for w in work if w[0] in exceptional]]
+            subs = [sb for sb in subs if sb]
+            lanes = [main] + side
+            for sd in side:
+                sd.wait_stream(main)
+            for i, sub in enumerate(subs):
+                with torch.cuda.stream(lanes[i % len(lanes)]):
+                    execute_plans([(plan, a, b, 1.0, 0.0, c) for cid, plan, a, b, c in sub])
+            for sd in side:
+                main.wait_stream(sd)
+            return
         for sd in side:
             sd.wait_stream(main)
         lanes = [main] + side
@@ -242,9 +302,11 @@ def run_gpu(args):
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream(device)
         cap.wait_stream(stream)
+        cap_launch0 = _lib.launch_count()
         with torch.cuda.stream(cap):
             with torch.cuda.graph(graph, stream=cap):
                 issue_step(cap)
+        launches_per_step = _lib.launch_count() - cap_launch0
         stream.wait_stream(cap)
         for _ in range(args.warmup):
             graph.replay()
@@ -263,7 +325,8 @@ def run_gpu(args):
                 issue_step(stream)
         t1e.record(stream)
         torch.cuda.synchronize()
-    launches = (_lib.launch_count() - launches0) if graph is None else nc * args.steps
+    launches = ((_lib.launch_count() - launches0) if graph is None
+                else launches_per_step * args.steps)
     barrier()
     total_ms = t0e.elapsed_time(t1e)
     kern_ms = sum(sum(x) for x in per_case)
@@ -310,6 +373,10 @@ def run_gpu(args):
         k = kernel_of[cid]
         fam_ms[k] = fam_ms.get(k, 0.0) + statistics.mean(per_case[i])
         fam_flops[k] = fam_flops.get(k, 0.0) + fl
+    if group_attr:
+        fam_ms = {k: v["ms"] for k, v in group_attr.items()}
+        fam_flops = {k: v["cases"] * fl for k, v in group_attr.items()}
+        kern_ms = sum(fam_ms.values()) * args.steps
     dom = max(fam_ms, key=fam_ms.get)
     dom_tflops = fam_flops[dom] / (fam_ms[dom] * 1e-3) / 1e12
     bound = "tensor" if fl / by > (peak_tflops * 1e12) / (hbm * 1e9) else "hbm"
@@ -329,7 +396,10 @@ def run_gpu(args):
                                 "B read, C written once; beta = 0)"},
         "step_frac_of_roofline": round(roof_ms / ms_per_step, 4),
         "kernel_share_of_step": round(fam_ms[dom] / (kern_ms / args.steps), 4),
-        "measured_in": "CUDA events on the launching stream, per-case pass without graph",
+        "measured_in": ("CUDA events on the launching stream around each grouped launch "
+                        "(plain cases / exceptional cases)" if group_attr else
+                        "CUDA events on the launching stream, per-case pass without graph"),
+        "per_launch_cases": (group_attr[dom]["cases"] if group_attr else 1),
     }
     per_case_out = {work[i][0]: {"ms": round(statistics.median(per_case[i]), 4),
                                  "kernel": kernel_of[work[i][0]],
@@ -356,13 +426,18 @@ def run_gpu(args):
                        "n": n, "cases": nc, "gflop_per_step_per_gpu": round(step_flops / 1e9, 2),
                        "parallelism": f"batch-sharded x{world} (no collective)",
                        "l2": "4 rotating operand sets, each > L2 (126 MB) at n>=256",
-                       "issue": f"36 independent launches per step, round-robin on {args.streams} stream(s)",
+                       "issue": ("one execute_plans call per step: the 36 independent "
+                                 "contractions as grouped persistent launches (plain / "
+                                 "exceptional)" if group else
+                                 f"36 independent launches per step, round-robin on "
+                                 f"{args.streams} stream(s)"),
                        "alpha": 1.0, "beta": 0.0},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "cuda_graph": graph is not None, "streams": args.streams,
+            "grouped": group, "group_launches": group_attr,
             "ms_per_step_nograph": round(nograph_ms, 4),
             "clocks": clocks.summary(),
             "wall_ms_timed_region": round(total_ms, 3),
@@ -673,6 +748,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--no-group", action="store_true",
+                    help="issue the cases as separate calls instead of one grouped call")
     ap.add_argument("--sustained-probe", action="store_true",
                     help="also measure the power-capped (sustained) TF32 peak (~3 s)")
     ap.add_argument("--config", choices=("sweep", "small", "order4", "hooi", "conventional"),

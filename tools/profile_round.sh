@@ -3,9 +3,11 @@
 # Reports stay in /tmp/prof on the box (too large to bring back); the counter
 # summaries land in gpurun_out/ (copied to profiles/ afterwards).
 mkdir -p gpurun_out /tmp/prof
-TAG=${TAG:-r01c}
+TAG=${TAG:-r01d}
 NCU="ncu --set full --clock-control none --import-source on"
 timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/pair_1.3_n256 -f python tools/case_single.py 1.3 256 f32 3 > /dev/null 2>&1
+timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/group_plain_n256 -f python tools/group_single.py plain 256 3 > /dev/null 2>&1
+timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/group_bb_n256 -f python tools/group_single.py bb 256 3 > /dev/null 2>&1
 timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/pairbb_6.4_n256 -f python tools/case_single.py 6.4 256 f32 3 > /dev/null 2>&1
 timeout 300 $NCU -k regex:dmma -s 2 -c 1 -o /tmp/prof/dmma_1.3_n256 -f python tools/case_single.py 1.3 256 f64 3 > /dev/null 2>&1
 timeout 300 $NCU -k regex:dmma -s 2 -c 1 -o /tmp/prof/dmma_bb_6.4_n256 -f python tools/case_single.py 6.4 256 f64 3 > /dev/null 2>&1
@@ -14,6 +16,8 @@ timeout 300 $NCU -k regex:small -s 1 -c 1 -o /tmp/prof/small32_f64 -f python too
 timeout 300 $NCU -k regex:pair_tma -s 1 -c 1 -o /tmp/prof/fold_order4 -f python bench.py --config order4 --steps 1 --warmup 3 > /dev/null 2>&1
 NCU_TRAFFIC_JSON=gpurun_out/ncu_traffic.json python tools/ncu_summary.py gpurun_out/${TAG}_ncu_summary.md \
   /tmp/prof/pair_1.3_n256.ncu-rep:tc_tf32x3_pair_tma/n256/f32 \
+  /tmp/prof/group_plain_n256.ncu-rep:tc_tf32x3_pair_group/n256/f32 \
+  /tmp/prof/group_bb_n256.ncu-rep:tc_tf32x3_pair_group_bb/n256/f32 \
   /tmp/prof/pairbb_6.4_n256.ncu-rep:tc_tf32x3_pair_bb/n256/f32 \
   /tmp/prof/dmma_1.3_n256.ncu-rep:tc_dmma_f64/n256/f64 \
   /tmp/prof/dmma_bb_6.4_n256.ncu-rep:tc_dmma_f64_bb/n256/f64 \

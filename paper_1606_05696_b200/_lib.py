@@ -103,6 +103,8 @@ def load():
                 "(there is no CPU fallback)")
         lib = ctypes.CDLL(str(LIB_PATH))
         for name, (args, res) in SIGNATURES.items():
+            if os.environ.get("SBT_LIB") and not hasattr(lib, name):
+                continue  # A/B experiments with an older build: tolerate new symbols
             fn = getattr(lib, name)  # AttributeError = missing export -> loud failure
             fn.argtypes = args
             fn.restype = res

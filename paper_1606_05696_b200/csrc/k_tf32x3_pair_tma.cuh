@@ -199,6 +199,12 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
   const Problem* __restrict__ prs = ps.pr;
   const int nprob = ps.n;
   const int64_t total = ps.total;
+  // problem of global tile t; a single-problem launch indexes ps.pr[0] at
+  // compile time so its fields stay in the constant bank / uniform registers
+  auto prob = [&](int64_t t, int& cur) -> const Problem& {
+    if constexpr (MAXP == 1) { (void)t; (void)cur; return ps.pr[0]; }
+    else return locate(prs, nprob, t, cur);
+  };
   using Gm = Geo<BK, BB, BNT>;
   constexpr int HNT = BNT / 2;  // B columns per CTA (MN-major B needs HNT >= 32: host-checked)
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
@@ -266,7 +272,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
         int am, ab, ab2, bn, bb, bb2;
       };
       auto decode = [&](int64_t tile_idx, int& cur) {
-        const Problem& P = locate(prs, nprob, tile_idx, cur);
+        const Problem& P = prob(tile_idx, cur);
         const GemmParams<float>& p = P.p;
         const Fold& f = P.f;
         const bool a_bc = p.aps == 0, a_bc2 = p.aps2 == 0, b_bc = p.bps == 0, b_bc2 = p.bps2 == 0;
@@ -364,7 +370,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     int64_t n_iter = 0;  // K-blocks of this pair's tiles
     {
       int cur = 0;
-      for (int64_t t = pair; t < total; t += npairs) n_iter += locate(prs, nprob, t, cur).nkb;
+      for (int64_t t = pair; t < total; t += npairs) n_iter += prob(t, cur).nkb;
     }
     for (int64_t g = grp; g < n_iter; g += kConvWarps / kGroupWarps) {
       const uint32_t s = uint32_t(g % RAW_SLOTS);
@@ -414,7 +420,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     uint32_t nchunk = 0, tcount = 0;
     int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-      const Problem& P = locate(prs, nprob, t, cur);
+      const Problem& P = prob(t, cur);
       const GemmParams<float>& p = P.p;
       const Fold& f = P.f;
       const Tile tc = tile_of<BB, BNT>(t - P.tile_begin, P.tiles_m, P.tiles_n, P.nbatch);
@@ -604,7 +610,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     uint32_t it = 0, tcount = 0;
     int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
-      const Problem& P = locate(prs, nprob, t, cur);
+      const Problem& P = prob(t, cur);
       const bool A_K = !BB && P.a_k, B_K = P.b_k;
       const int nkb = P.nkb;
       const uint32_t idesc = ptx::idesc_tf32(BM, BNT, !A_K, !B_K);

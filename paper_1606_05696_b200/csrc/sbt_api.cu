@@ -124,23 +124,26 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
     if (kernel_override() == 0) {
       // bucket the pair-kernel problems by configuration (bb, split, bnt)
       std::vector<PairPlan> plans(count);
-      std::vector<int> buckets[10];
+      std::vector<int> buckets[12];
       for (int i = 0; i < count; ++i) {
         const GemmParams<float>& p = ps[i];
         if (p.batch == 0 || p.batch2 == 0) { launched[i] = 1; continue; }
         if (p.k > kMaxChunkK) continue;                       // K-chunked: single path
         if (!plan_pair(p, &plans[i])) continue;
         const PairPlan& pl = plans[i];
-        const int key = pl.bb ? (pl.split ? 9 : 8)
+        const int key = pl.bb ? (8 + (pl.bnt == 128 ? 2 : 0) + (pl.split ? 1 : 0))
                               : ((pl.bnt == 32 ? 0 : pl.bnt == 64 ? 1 : pl.bnt == 128 ? 2 : 3) * 2 +
                                  (pl.split ? 1 : 0));
         buckets[key].push_back(i);
       }
-      for (int key = 0; key < 10; ++key) {
+      for (int key = 0; key < 12; ++key) {
         if (buckets[key].empty()) continue;
         const PairPlan& pl0 = plans[buckets[key][0]];
         int rc;
-        if (pl0.bb) {
+        if (pl0.bb && pl0.bnt == 128) {
+          rc = pl0.split ? GroupRun<true, true, 128>::run(plans, buckets[key], stream, launched)
+                         : GroupRun<false, true, 128>::run(plans, buckets[key], stream, launched);
+        } else if (pl0.bb) {
           rc = pl0.split ? GroupRun<true, true, 256>::run(plans, buckets[key], stream, launched)
                          : GroupRun<false, true, 256>::run(plans, buckets[key], stream, launched);
         } else {

@@ -168,12 +168,13 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
       if (p.ars < 4 || p.acs < 4 || !vmult<float>(p.ars) || !vmult<float>(p.acs) ||
           !vmult<float>(p.aps2))
         continue;
-      if (p.m < 64 || p.n < 192) continue;
+      if (p.m < 64 || p.n < 96) continue;
       const int bm = b_major(p);
       if (!bm) continue;
       out->p = p;
       out->f = tf32tma::Fold{p.m, p.n, p.m, p.n, 0, 0, 0};
-      out->am = 2; out->bm = bm; out->bb = true; out->bnt = 256; out->split = pick_split(p);
+      out->am = 2; out->bm = bm; out->bb = true; out->bnt = p.n < 192 ? 128 : 256;
+      out->split = pick_split(p);
       return true;
     }
     if (variant == 5) return false;
@@ -304,7 +305,11 @@ static int launch_pair_single_t(const PairPlan& pl, cudaStream_t stream) {
 // dispatch on the compile-time configuration of a plan
 template <template <bool, bool, int> class F, typename... Args>
 static int with_pair_cfg(const PairPlan& pl, Args&&... args) {
-  if (pl.bb) return pl.split ? F<true, true, 256>::run(args...) : F<false, true, 256>::run(args...);
+  if (pl.bb) {
+    if (pl.bnt == 128)
+      return pl.split ? F<true, true, 128>::run(args...) : F<false, true, 128>::run(args...);
+    return pl.split ? F<true, true, 256>::run(args...) : F<false, true, 256>::run(args...);
+  }
   switch (pl.bnt) {
     case 32: return pl.split ? F<true, false, 32>::run(args...) : F<false, false, 32>::run(args...);
     case 64: return pl.split ? F<true, false, 64>::run(args...) : F<false, false, 64>::run(args...);

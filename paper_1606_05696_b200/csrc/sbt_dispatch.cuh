@@ -20,6 +20,7 @@
 #include "k_dmma.cuh"
 #include "k_small.cuh"
 #include "k_small_dmma.cuh"
+#include "k_small64.cuh"
 #include "k_gemv.cuh"
 #include "sbt_tma.cuh"
 
@@ -553,6 +554,37 @@ static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
   return 1;
 }
 
+// fp32 64 x 64 x 64 batches with column-major A, B and C: 8 x 8 register blocks.
+static int try_small64(const GemmParams<float>& p, cudaStream_t stream) {
+  using namespace small64;
+  if (p.m != 64 || p.n != 64 || p.k != 64) return 0;
+  if (!(p.ars == 1 && p.acs == 64 && p.brs == 1 && p.bcs == 64 && p.crs == 1 && p.ccs == 64))
+    return 0;
+  if (p.aps % 4 || p.bps % 4 || p.aps < 4096 || p.bps < 4096 || !aligned16(p.a) ||
+      !aligned16(p.b) || p.batch > (int64_t(1) << 31))
+    return 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(small64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess)
+      return -3;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_tmap_f32(&ta, p.a, 64, 64, 64, p.batch, p.aps, 1, 0, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, G) ||
+      !make_tmap_f32(&tb, p.b, 64, 64, 64, p.batch, p.bps, 1, 0, LDB, 64,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, G))
+    return 0;
+  const int64_t ngroups = ceil_div(p.batch, G);
+  const int64_t cap = int64_t(kNumSMs) * CTAS_PER_SM;
+  const int64_t grid = ngroups < cap ? ngroups : cap;
+  small64_kernel<<<dim3(unsigned(grid)), dim3(kThreads), SMEM_BYTES, stream>>>(p, ta, tb,
+                                                                              ngroups);
+  note_launch("small64_f32");
+  return 1;
+}
+
 // Many tiny dense matrices: every extent <= 64, each matrix stored densely.
 template <typename T>
 static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
@@ -565,6 +597,13 @@ static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
   if (!vmult<T>(p.m * p.k) || !vmult<T>(p.k * p.n) || !vmult<T>(p.aps) || !vmult<T>(p.bps) ||
       !aligned16(p.a) || !aligned16(p.b))
     return 0;
+  if constexpr (sizeof(T) == 4) {
+    static const int use64 = env_int("SBT_SMALL64", 1);
+    if (use64 && mx == 64) {
+      const int rc = try_small64(p, stream);
+      if (rc != 0) return rc;
+    }
+  }
   if constexpr (sizeof(T) == 8) {
     static const int use_dmma = env_int("SBT_SMALL_DMMA", 1);
     if (use_dmma && mx > 16 && mx <= 32) {

@@ -1,0 +1,489 @@
+// Rayleigh-Ritz step of the HOOI eigensolver, entirely on the device.
+//
+// The reference takes the leading `rank` eigenvectors of each mode's Gram
+// matrix (tucker.py:63-76, Jacobi on the full n x n Gram, tucker.py:21-60).
+// HOOI here runs one warm-started subspace sweep per factor (tucker.py
+// top_eigh): Q = previous factor (n x p), Z = G Q, and M = [Q Z]^T Z give the
+// projected matrix H = Q^T G Q (p x p).  This kernel finishes the sweep
+// without a host round trip, so a whole HOOI iteration is launch-only:
+//   * cyclic Jacobi on H in shared memory (round-robin pairing: the p/2
+//     rotations of a step are independent, so a step is A <- J^T A J with J a
+//     product of disjoint rotations).  The index pairs of a step partition
+//     A and V into 2 x 2 blocks, each updated in place by one thread (A's
+//     upper triangle of blocks only, mirrored): 8 shared-memory loads and
+//     stores per 4 elements -- the fp64 step is shared-memory bound;
+//   * Ritz vectors from row tiles of Q and Z staged in shared memory (all
+//     loads of a tile in flight at once);
+//   * eigenvalues sorted descending;
+//   * U = Q V, Y = Z V (= G U) for the leading `rank` Ritz vectors;
+//   * residuals ||Y_j - w_j U_j|| and the convergence flag
+//     max_j ||.|| <= tol * w_max (the same test as top_eigh);
+//   * sign rule of tucker.py:71-75 (largest |entry| of each column positive,
+//     first index on ties).
+// One CTA; p <= kMaxP.  The caller checks `flag` later (once per iteration)
+// and redoes the iteration on the host path if any factor did not converge.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "sbt_common.cuh"
+
+namespace sbt {
+namespace ritz {
+
+#ifdef SBT_RITZ_CLOCK
+__device__ long long g_ritz_clock[2];  // [1]: cycles of the Jacobi steps
+#endif
+constexpr int kMaxP = 64;
+constexpr int kHalf = kMaxP / 2;
+constexpr int kThreads = 512;
+constexpr int kCluster = 8;                    // CTAs sharing the Ritz-vector phase
+constexpr int LDS = kMaxP + 1;
+constexpr int MAT = kMaxP * LDS;               // one P x P matrix (padded rows)
+constexpr int kTileRows = 64;                  // Ritz-vector phase row tile
+constexpr int REGION0 = (5 * MAT > 2 * kTileRows * kMaxP) ? 5 * MAT : 2 * kTileRows * kMaxP;
+constexpr int kTri = kHalf * (kHalf + 1) / 2;  // upper-triangular 2 x 2 blocks
+constexpr int SMEM_BYTES =
+    (REGION0 + 4 * kMaxP) * 8 + (2 * kMaxP) * 4 + (kMaxP * kMaxP + 2 * kTri) + 64;
+
+// C = op(X) Y for P x P matrices in shared memory (row stride LDS), 2 x 2
+// register blocks per thread; EPI 1 stores 1.5 I - 0.5 C (Newton-Schulz).
+template <bool TX, int EPI>
+__device__ __forceinline__ void small_mm(const double* X, const double* Y, double* C, int P,
+                                         int tid) {
+  const int hb = P / 2;
+  for (int blk = tid; blk < hb * hb; blk += kThreads) {
+    const int i0 = 2 * (blk / hb), j0 = 2 * (blk % hb);
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    for (int l = 0; l < P; ++l) {
+      const double x0 = TX ? X[l * LDS + i0] : X[i0 * LDS + l];
+      const double x1 = TX ? X[l * LDS + i0 + 1] : X[(i0 + 1) * LDS + l];
+      const double y0 = Y[l * LDS + j0], y1 = Y[l * LDS + j0 + 1];
+      c00 = fma(x0, y0, c00);
+      c01 = fma(x0, y1, c01);
+      c10 = fma(x1, y0, c10);
+      c11 = fma(x1, y1, c11);
+    }
+    if (EPI == 1) {
+      c00 = (i0 == j0 ? 1.5 : 0.0) - 0.5 * c00;
+      c01 = -0.5 * c01;
+      c10 = -0.5 * c10;
+      c11 = (i0 == j0 ? 1.5 : 0.0) - 0.5 * c11;
+    }
+    C[i0 * LDS + j0] = c00;
+    C[i0 * LDS + j0 + 1] = c01;
+    C[(i0 + 1) * LDS + j0] = c10;
+    C[(i0 + 1) * LDS + j0 + 1] = c11;
+  }
+}
+
+// qz: [Q | Z] stored as 2p rows of length n (row j = column j of Q, then of Z);
+// m: the (2p x p) column-major product [Q Z]^T Z (ld 2p).
+// ut: rank rows of length n (U column-major); yt (optional): the same for
+// Y = G U (the next sweep's basis, before the sign rule); w: rank eigenvalues
+// (descending); flag[0] = converged; rel[0] = max residual / w_max,
+// rel[1] = Jacobi sweeps, rel[2..4] = SM cycles of the eigen / Ritz-vector /
+// sign phases, rel[5] = Newton refinement steps (diagnostics).
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
+ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t n, int p,
+            int rank, double tol, double* __restrict__ ut, double* __restrict__ yt,
+            double* __restrict__ w, int* __restrict__ flag, double* __restrict__ rel) {
+  extern __shared__ __align__(16) double smr[];
+  // eigen phase: A double-buffered at smr + {0, 1} * MAT (buffer 1 is W in the
+  // Newton phase), V at smr + 2 * MAT, H at smr + 3 * MAT, S at smr + 4 * MAT
+  double* V = smr + 2 * MAT;
+  double* H = smr + 3 * MAT;
+  double* S = smr + 4 * MAT;
+  double* W = smr + MAT;
+  double* Qs = smr;                     // [p][kTileRows] (Ritz phase, reuses A / V)
+  double* Zs = smr + kTileRows * kMaxP;
+  double* Vs = smr + 4 * MAT;           // [p][LDS]: sorted leading eigenvectors (reuses S)
+  double* wv = smr + REGION0;           // sorted eigenvalues
+  double* res = wv + kMaxP;             // [rank] squared residuals
+  double* amax = res + kMaxP;           // [rank] max |U| per column
+  double* sgn = amax + kMaxP;           // [rank] sign rule
+  int* perm = reinterpret_cast<int*>(sgn + kMaxP);               // perm[j] = index of the j-th largest
+  int* s_arg = perm + kMaxP;            // first row attaining amax
+  unsigned char* pairs = reinterpret_cast<unsigned char*>(s_arg + kMaxP);  // [P-1][P]
+  unsigned char* tri = pairs + kMaxP * kMaxP;                               // [kTri][2]
+  __shared__ double s_red[2];
+  __shared__ int s_clamp;
+  const int tid = threadIdx.x;
+  const long long t_start = clock64();
+  const int P = p + (p & 1);            // even; a padding index is decoupled
+  const int half = P / 2;
+  const int ntri = half * (half + 1) / 2;
+  const int nitems = ntri + half * half;  // A blocks (i <= j) + V blocks
+  const int64_t ldm = 2 * int64_t(p);
+
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = int(cluster.block_rank());
+  int sweeps = 0, newton = 0;
+  long long t_jacobi = t_start;
+  if (crank == 0) {  // the eigen phase runs on CTA 0; the others wait
+    // round-robin schedule (circle method: position 0 holds player P-1) and
+    // the upper-triangular block list
+    for (int e = tid; e < (P - 1) * half; e += kThreads) {
+      const int step = e / half, i = e % half;
+      auto idx = [&](int pos) { return pos == 0 ? P - 1 : (pos - 1 + step) % (P - 1); };
+      pairs[step * P + 2 * i] = (unsigned char)idx(i);
+      pairs[step * P + 2 * i + 1] = (unsigned char)idx(P - 1 - i);
+    }
+    if (tid < half) {
+      int base = tid * half - tid * (tid - 1) / 2;  // blocks (tid, tid..half-1)
+      for (int j = tid; j < half; ++j, ++base) {
+        tri[2 * base] = (unsigned char)tid;
+        tri[2 * base + 1] = (unsigned char)j;
+      }
+    }
+    if (tid < 2) s_red[tid] = 0.0;
+    __syncthreads();
+    double fro = 0.0;
+    for (int e = tid; e < P * P; e += kThreads) {
+      const int i = e / P, j = e % P;
+      double h = 0.0;
+      if (i < p && j < p) h = 0.5 * (m[i + j * ldm] + m[j + i * ldm]);
+      smr[i * LDS + j] = h;
+      H[i * LDS + j] = h;
+      V[i * LDS + j] = i == j ? 1.0 : 0.0;
+      fro += h * h;
+    }
+    for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+    if ((tid & 31) == 0) atomicAdd(&s_red[0], fro);
+    __syncthreads();
+    // rotate only while |a_pq| > floor: the residual test is relative to w_max,
+    // so off-diagonal mass far below tol * ||H|| changes no decision (a test
+    // relative to sqrt(a_pp a_qq) would keep rotating rounding noise between the
+    // smallest Ritz values)
+    const double floor_abs = fmax(1e-15, 1e-3 * tol) * sqrt(s_red[0]);
+    // rotation of pair (a, b) from the current A: J[a][a] = J[b][b] = c,
+    // J[a][b] = s, J[b][a] = -s.  t = tan(angle) at float precision (any t
+    // gives an orthogonal rotation; |th| <= 2e15 above the floor), c = (1 +
+    // t^2)^-1/2 by two fp64 Newton steps from the float estimate.  Every
+    // thread that needs a rotation computes it from the same inputs.
+    auto rot = [&](const double* Ao, int a, int b, double& c, double& sn) {
+      const double apq = Ao[a * LDS + b];
+      c = 1.0;
+      sn = 0.0;
+      if (fabs(apq) > floor_abs) {
+        const double app = Ao[a * LDS + a], aqq = Ao[b * LDS + b];
+        const float th = __fdividef(float(aqq - app), float(2.0 * apq));
+        const float tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
+        const double t = double(tf), v = fma(t, t, 1.0);
+        double x = double(rsqrtf(float(v)));
+        x = x * fma(-0.5 * v, x * x, 1.5);
+        x = x * fma(-0.5 * v, x * x, 1.5);
+        c = x;
+        sn = t * x;
+      }
+    };
+    // Newton refinement for a warm start (H nearly diagonal): with A = V^T H V,
+    // V <- V (I + E), E_ij = A_ij / (A_jj - A_ii) (antisymmetric: annihilates
+    // A's off-diagonal to first order), re-orthonormalised by one Newton-Schulz
+    // step V <- W (1.5 I - 0.5 W^T W).  Quadratic convergence in a handful of
+    // small matrix products instead of (p-1)-step Jacobi sweeps; pairs too
+    // close for the first-order update (|A_ij| > |A_jj - A_ii| / 4) hand over
+    // to the Jacobi sweeps below, which also finish anything left.
+    for (int itn = 0; itn < 4; ++itn) {
+      if (tid == 0) s_red[1] = 0.0, s_clamp = 0;
+      __syncthreads();
+      double off = 0.0;
+      int clamp = 0;
+      for (int e = tid; e < P * P; e += kThreads) {
+        const int i = e / P, j = e % P;
+        double x = 1.0;
+        if (i != j) {
+          const double a = smr[i * LDS + j], d = smr[j * LDS + j] - smr[i * LDS + i];
+          off = fmax(off, fabs(a));
+          x = 0.0;
+          if (fabs(a) > floor_abs) {
+            if (fabs(a) <= 0.25 * fabs(d)) x = a / d;
+            else clamp = 1;
+          }
+        }
+        S[i * LDS + j] = x;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
+        clamp |= __shfl_xor_sync(0xffffffffu, clamp, o);
+      }
+      if ((tid & 31) == 0) {
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_red[1]), __double_as_longlong(off));
+        if (clamp) atomicOr(&s_clamp, 1);
+      }
+      __syncthreads();
+      if (s_red[1] <= floor_abs || s_clamp) break;
+      ++newton;
+      small_mm<false, 0>(V, S, W, P, tid);   // W = V (I + E)
+      __syncthreads();
+      small_mm<true, 1>(W, W, S, P, tid);    // S = 1.5 I - 0.5 W^T W
+      __syncthreads();
+      small_mm<false, 0>(W, S, V, P, tid);   // V = W S
+      __syncthreads();
+      small_mm<false, 0>(H, V, W, P, tid);   // W = H V
+      __syncthreads();
+      small_mm<true, 0>(V, W, smr, P, tid);  // A = V^T H V
+      __syncthreads();
+      for (int e = tid; e < P * P; e += kThreads) {
+        const int i = e / P, j = e % P;
+        if (i < j) {
+          const double a = 0.5 * (smr[i * LDS + j] + smr[j * LDS + i]);
+          smr[i * LDS + j] = a;
+          smr[j * LDS + i] = a;
+        }
+      }
+      __syncthreads();
+    }
+    int cur = 0;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      // converged when no off-diagonal element exceeds the floor
+      const double* Ac = smr + cur * MAT;
+      double off = 0.0;
+      for (int e = tid; e < P * P; e += kThreads) {
+        const int i = e / P, j = e % P;
+        if (i != j) off = fmax(off, fabs(Ac[i * LDS + j]));
+      }
+      for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
+      if (tid == 0) s_red[1] = 0.0;
+      __syncthreads();
+      if ((tid & 31) == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_red[1]), __double_as_longlong(off));
+      __syncthreads();
+      if (s_red[1] <= floor_abs) break;
+      ++sweeps;
+      for (int step = 0; step < P - 1; ++step) {
+  #ifdef SBT_RITZ_CLOCK
+        const long long c0 = clock64();
+  #endif
+        // one barrier per step: rotations and blocks read A (buffer cur), the
+        // new A goes to the other buffer; V is updated in place (each V block
+        // belongs to one thread and V is not read by the rotations)
+        const double* Ao = smr + cur * MAT;
+        double* An = smr + (cur ^ 1) * MAT;
+        const unsigned char* pr = pairs + step * P;
+        for (int it = tid; it < nitems; it += kThreads) {
+          if (it < ntri) {          // A block (i, j), i <= j, and its mirror
+            const int i = tri[2 * it], j = tri[2 * it + 1];
+            const int ai = pr[2 * i], bi = pr[2 * i + 1], aj = pr[2 * j], bj = pr[2 * j + 1];
+            double ci, si, cj, sj;
+            rot(Ao, ai, bi, ci, si);
+            if (i == j) cj = ci, sj = si;
+            else rot(Ao, aj, bj, cj, sj);
+            const double x00 = Ao[ai * LDS + aj], x01 = Ao[ai * LDS + bj];
+            const double x10 = Ao[bi * LDS + aj], x11 = Ao[bi * LDS + bj];
+            // J_i^T X
+            const double y00 = ci * x00 - si * x10, y01 = ci * x01 - si * x11;
+            const double y10 = si * x00 + ci * x10, y11 = si * x01 + ci * x11;
+            // (J_i^T X) J_j
+            const double z00 = y00 * cj - y01 * sj, z01 = y00 * sj + y01 * cj;
+            const double z10 = y10 * cj - y11 * sj, z11 = y10 * sj + y11 * cj;
+            An[ai * LDS + aj] = z00;
+            An[ai * LDS + bj] = z01;
+            An[bi * LDS + aj] = z10;
+            An[bi * LDS + bj] = z11;
+            if (i != j) {
+              An[aj * LDS + ai] = z00;
+              An[bj * LDS + ai] = z01;
+              An[aj * LDS + bi] = z10;
+              An[bj * LDS + bi] = z11;
+            }
+          } else {                  // V block: rows of pair i, columns of pair j
+            const int r = it - ntri, i = r / half, j = r % half;
+            const int ai = pr[2 * i], bi = pr[2 * i + 1], aj = pr[2 * j], bj = pr[2 * j + 1];
+            double cj, sj;
+            rot(Ao, aj, bj, cj, sj);
+            if (sj == 0.0) continue;
+            const double v00 = V[ai * LDS + aj], v01 = V[ai * LDS + bj];
+            const double v10 = V[bi * LDS + aj], v11 = V[bi * LDS + bj];
+            V[ai * LDS + aj] = v00 * cj - v01 * sj;
+            V[ai * LDS + bj] = v00 * sj + v01 * cj;
+            V[bi * LDS + aj] = v10 * cj - v11 * sj;
+            V[bi * LDS + bj] = v10 * sj + v11 * cj;
+          }
+        }
+        cur ^= 1;
+        __syncthreads();
+  #ifdef SBT_RITZ_CLOCK
+        if (tid == 0) g_ritz_clock[1] += clock64() - c0;
+  #endif
+      }
+    }
+    const double* A = smr + cur * MAT;
+    t_jacobi = clock64();
+
+    // descending order of the p true eigenvalues (the padding index is excluded)
+    if (tid < p) {
+      const double d = A[tid * LDS + tid];
+      int pos = 0;
+      for (int j = 0; j < p; ++j) {
+        const double dj = A[j * LDS + j];
+        pos += (dj > d) || (dj == d && j < tid);
+      }
+      perm[pos] = tid;
+    }
+    if (tid < kMaxP) {
+      res[tid] = 0.0;
+      amax[tid] = 0.0;
+      s_arg[tid] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int e = tid; e < p * rank; e += kThreads) {
+      const int l = e / rank, j = e % rank;
+      Vs[l * LDS + j] = V[l * LDS + perm[j]];
+    }
+    if (tid < rank) {
+      wv[tid] = A[perm[tid] * LDS + perm[tid]];
+      w[tid] = wv[tid];
+    }
+  }
+  // ---- Ritz vectors, residuals and sign rule on all CTAs of the cluster ----
+  cluster.sync();
+  if (crank != 0) {  // copy the sorted eigenvectors / values from CTA 0
+    const double* rVs = cluster.map_shared_rank(Vs, 0);
+    const double* rwv = cluster.map_shared_rank(wv, 0);
+    for (int e = tid; e < p * rank; e += kThreads) {
+      const int l = e / rank, j = e % rank;
+      Vs[l * LDS + j] = rVs[l * LDS + j];
+    }
+    if (tid < rank) wv[tid] = rwv[tid];
+  }
+  if (tid < kMaxP) {
+    res[tid] = 0.0;
+    amax[tid] = 0.0;
+    s_arg[tid] = 0x7fffffff;
+  }
+  __syncthreads();  // A / V are dead from here: region 0 holds Q / Z tiles
+  const double wmax = fmax(wv[0], 0.0);
+
+  // U = Q V_r, Y = Z V_r over row tiles (tile t on CTA t % kCluster);
+  // thread = (row r, 8-column group g)
+  const double* Q = qz;
+  const double* Z = qz + int64_t(p) * n;
+  const int r = tid % kTileRows, g = tid / kTileRows;  // 8 groups of 8 columns
+  const int ngroups = (rank + 7) / 8;
+  double rsum[8], mx[8];
+  int ax[8];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) rsum[jj] = 0.0, mx[jj] = -1.0, ax[jj] = 0x7fffffff;
+  for (int64_t i0 = int64_t(crank) * kTileRows; i0 < n; i0 += kCluster * kTileRows) {
+    const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
+    for (int e = tid; e < p * kTileRows; e += kThreads) {
+      const int l = e / kTileRows, rr = e % kTileRows;
+      const bool in = rr < rows;
+      Qs[l * kTileRows + rr] = in ? Q[int64_t(l) * n + i0 + rr] : 0.0;
+      Zs[l * kTileRows + rr] = in ? Z[int64_t(l) * n + i0 + rr] : 0.0;
+    }
+    __syncthreads();
+    if (g < ngroups) {
+      const int j0 = 8 * g;
+      double u[8], y[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) u[jj] = y[jj] = 0.0;
+      for (int l = 0; l < p; ++l) {
+        const double q = Qs[l * kTileRows + r], z = Zs[l * kTileRows + r];
+        const double* vr = Vs + l * LDS + j0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          u[jj] = fma(q, vr[jj], u[jj]);
+          y[jj] = fma(z, vr[jj], y[jj]);
+        }
+      }
+      if (r < rows) {
+        const int64_t i = i0 + r;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (j0 + jj >= rank) break;
+          const double d = y[jj] - wv[j0 + jj] * u[jj];
+          rsum[jj] = fma(d, d, rsum[jj]);
+          const double au = fabs(u[jj]);
+          if (au > mx[jj]) mx[jj] = au, ax[jj] = int(i);  // i ascending
+          ut[int64_t(j0 + jj) * n + i] = u[jj];
+          if (yt) yt[int64_t(j0 + jj) * n + i] = y[jj];
+        }
+      }
+    }
+    __syncthreads();  // the tile buffers are reused
+  }
+  // per-CTA column reductions: residual sums, then (max |u|, first index)
+  if (g < ngroups) {  // warp-uniform (a warp shares g)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = 8 * g + jj;
+      if (j >= rank) break;
+      double rr = rsum[jj], a = mx[jj];
+      int x = ax[jj];
+      for (int o = 16; o > 0; o >>= 1) {
+        rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        const double ao = __shfl_xor_sync(0xffffffffu, a, o);
+        const int xo = __shfl_xor_sync(0xffffffffu, x, o);
+        if (ao > a || (ao == a && xo < x)) a = ao, x = xo;
+      }
+      if ((tid & 31) == 0) {
+        atomicAdd(&res[j], rr);
+        // max first (a >= 0: bit order == value order), then the smallest
+        // index attaining it
+        if (a >= 0.0)
+          atomicMax(reinterpret_cast<unsigned long long*>(&amax[j]), __double_as_longlong(a));
+      }
+      mx[jj] = a;
+      ax[jj] = x;
+    }
+  }
+  __syncthreads();
+  if (g < ngroups) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = 8 * g + jj;
+      if (j >= rank) break;
+      if ((tid & 31) == 0 && mx[jj] == amax[j]) atomicMin(&s_arg[j], ax[jj]);
+    }
+  }
+  __threadfence();  // U entries (global) visible to the cluster after the barrier
+  cluster.sync();
+  const long long t_ritz = clock64();
+  // sign rule (tucker.py:71-75): combine the CTAs' (max, first index) per
+  // column, then every CTA negates its own rows of negative columns
+  if (tid < rank) {
+    double best = -1.0;
+    int arg = 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < kCluster; ++c) {
+      const double a = *cluster.map_shared_rank(amax + tid, c);
+      const int x = *cluster.map_shared_rank(s_arg + tid, c);
+      if (a > best || (a == best && x < arg)) best = a, arg = x;
+    }
+    sgn[tid] = ut[int64_t(tid) * n + arg] < 0.0 ? -1.0 : 1.0;
+  }
+  cluster.sync();  // every CTA has read its reference entries before any negation
+  for (int64_t i0 = int64_t(crank) * kTileRows; i0 < n; i0 += kCluster * kTileRows) {
+    const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
+    for (int e = tid; e < rank * kTileRows; e += kThreads) {
+      const int j = e / kTileRows, rr = e % kTileRows;
+      if (rr < rows && sgn[j] < 0.0) ut[int64_t(j) * n + i0 + rr] *= -1.0;
+    }
+  }
+  if (crank == 0 && tid < 32) {  // one warp: residual norms and the flag
+    double rmax = 0.0;
+    for (int j = tid; j < rank; j += 32) {
+      double rj = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) rj += *cluster.map_shared_rank(res + j, c);
+      rmax = fmax(rmax, sqrt(rj));
+    }
+    for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    if (tid == 0) {
+      const bool ok = wmax > 0.0 && rmax <= tol * wmax;
+      flag[0] = ok ? 1 : 0;
+      rel[0] = wmax > 0.0 ? rmax / wmax : 0.0;
+      rel[1] = double(sweeps);
+      rel[2] = double(t_jacobi - t_start);  // diagnostics: SM cycles per phase
+      rel[3] = double(t_ritz - t_jacobi);
+      rel[4] = double(clock64() - t_ritz);
+      rel[5] = double(newton);
+    }
+  }
+  cluster.sync();  // no CTA exits while its shared memory may still be read
+}
+
+}  // namespace ritz
+}  // namespace sbt

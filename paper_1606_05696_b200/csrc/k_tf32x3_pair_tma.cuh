@@ -270,6 +270,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       struct Coord {
         const Problem* pr;
         int am, ab, ab2, bn, bb, bb2;
+        int qm[4], qb[4], qb2[4];  // MN-major A: the four 32-row boxes (fold per box)
       };
       auto decode = [&](int64_t tile_idx, int& cur) {
         const Problem& P = prob(tile_idx, cur);
@@ -299,6 +300,19 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
         }
         c.am = int(am); c.ab = a_bc ? 0 : int(ab); c.ab2 = a_bc2 ? 0 : int(ab2);
         c.bn = int(bn); c.bb = b_bc ? 0 : int(bb); c.bb2 = b_bc2 ? 0 : int(bb2);
+        // MN-major A loads 32-row boxes: with a fold of m_in < 128 rows (a
+        // multiple of 32) consecutive boxes belong to different batch entries
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int64_t qm = am + 32 * q, qx = 0;
+          if (f.fm && qm >= f.m_in) {
+            qx = qm / f.m_in;
+            qm -= qx * f.m_in;
+          }
+          c.qm[q] = int(qm);
+          c.qb[q] = (f.fm == 1 && !a_bc) ? int(ab + qx) : c.ab;
+          c.qb2[q] = (f.fm == 2 && !a_bc2) ? int(ab2 + qx) : c.ab2;
+        }
         return c;
       };
       // issue the TMA boxes of one K-block: into raw slot st (PF = false) or
@@ -312,8 +326,14 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
             if (PF) ptx::tma_prefetch_4d(tmA, c.ab, c.am + 8 * q, k0, c.ab2);
             else ptx::tma_load_4d(st + q * (BK * 128), tmA, bar, c.ab, c.am + 8 * q, k0, c.ab2);
           }
-        } else {
-          tma_operand<BK, PF>(c.pr->a_k, tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
+        } else if (c.pr->a_k) {
+          tma_operand<BK, PF>(true, tmA, st, bar, c.am, k0, c.ab, c.ab2, false, false);
+        } else {  // MN-major A: four 32-row boxes [32 m][BK k]
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (PF) ptx::tma_prefetch_4d(tmA, c.qm[q], k0, c.qb[q], c.qb2[q]);
+            else ptx::tma_load_4d(st + q * (BK * 128), tmA, bar, c.qm[q], k0, c.qb[q], c.qb2[q]);
+          }
         }
         tma_operand<BK, PF, HNT>(c.pr->b_k, &c.pr->tb, st + Gm::A_BYTES, bar, c.bn, k0, c.bb,
                                  c.bb2, false, false);

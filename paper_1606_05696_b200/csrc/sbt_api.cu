@@ -22,6 +22,7 @@
 #include "sbt_dispatch.cuh"
 #include "k_probe.cuh"
 #include "k_permute.cuh"
+#include "k_ritz.cuh"
 
 namespace sbt {
 
@@ -446,5 +447,28 @@ int sbt_permute_f32(int order, const int64_t* dims, const float* src, const int6
 
 SBT_DEFINE(double, f64)
 SBT_DEFINE(float, f32)
+
+// Rayleigh-Ritz finish of one warm-started subspace sweep (HOOI factor
+// update, reference tucker.py:63-76); see k_ritz.cuh.  Asynchronous: the
+// convergence flag is read by the caller later.
+int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, double tol,
+                 double* ut, double* yt, double* w, int* flag, double* rel, void* stream) {
+  if (!qz || !m || !ut || !w || !flag || !rel || n < 1 || p < 1 || p > ritz::kMaxP ||
+      rank < 1 || rank > p || p > n)
+    return fail(SBT_EINVAL, "sbt_ritz_f64: bad arguments");
+  static bool attr = false;
+  if (!attr) {
+    const int rc = check_cuda(cudaFuncSetAttribute(ritz::ritz_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   ritz::SMEM_BYTES),
+                              "cudaFuncSetAttribute");
+    if (rc != SBT_OK) return rc;
+    attr = true;
+  }
+  ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+      qz, m, n, p, rank, tol, ut, yt, w, flag, rel);
+  note_launch("ritz");
+  return check_cuda(cudaGetLastError(), "ritz launch");
+}
 
 }  // extern "C"

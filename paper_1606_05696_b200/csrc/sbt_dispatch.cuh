@@ -114,12 +114,15 @@ static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
 // Fold a batch mode into M (only A and C depend on it) and / or into N (only B
 // and C) when the extent is a multiple of the CTA block but not of the 256-wide
 // pair tile (see k_tf32x3_pair_tma.cuh, struct Fold).
-static tf32tma::Fold make_fold(const GemmParams<float>& p) {
+static tf32tma::Fold make_fold(const GemmParams<float>& p, bool a_mn) {
   tf32tma::Fold f{p.m, p.n, p.m, p.n, 0, 0, 0};
   auto cnt = [&](int w) { return w == 1 ? p.batch : p.batch2; };
   auto as = [&](int w) { return w == 1 ? p.aps : p.aps2; };
   auto bs = [&](int w) { return w == 1 ? p.bps : p.bps2; };
-  if (p.m % tf32tma::BM != 0 && p.m % tf32tma::HM == 0) {
+  // M folds need whole A boxes per batch entry: 128 rows for K-major A, 32
+  // for MN-major A (its boxes are 32-row MN atoms, each with its own batch)
+  const int64_t m_unit = a_mn ? 32 : tf32tma::HM;
+  if (p.m % tf32tma::BM != 0 && p.m % m_unit == 0) {
     for (int w : {2, 1})
       if (cnt(w) > 1 && bs(w) == 0 && as(w) > 0 && vmult<float>(as(w))) {
         f.fm = w;
@@ -188,7 +191,7 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
     const int qa = a_major(q), qb = b_major(q);
     if (!qa || !qb) continue;
     const tf32tma::Fold f =
-        variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q);
+        variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q, qa == 2);
     // narrow N (< 96) only pays off for many M rows in total (HBM-bound skinny
     // products: rank-r Tucker mode products); narrow tiles need K-major B
     const int64_t rows = f.mtot * ((f.fm == 1 || f.fn == 1) ? 1 : q.batch) *
@@ -234,8 +237,9 @@ static bool fill_problem(const PairPlan& pl, tf32tma::Problem* pr) {
   std::memset(&pr->tc, 0, sizeof(pr->tc));
   f.cmode = 0;
   static const int tma_epi = env_int("SBT_TC_TMA_EPI", 1);
+  // (128-row store boxes: not with an M fold of fewer rows per batch entry)
   if (!BB && tma_epi && p.beta == 0.f && aligned16(p.c) && vmult<float>(p.cps) &&
-      vmult<float>(p.cps2)) {
+      vmult<float>(p.cps2) && !(f.fm && f.m_in % tf32tma::HM != 0)) {
     if (p.crs == 1 && vmult<float>(p.ccs) &&
         make_tmap_f32(&pr->tc, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 128, 32,
                       CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -482,7 +486,10 @@ static int try_tensor_f32(const GemmParams<float>& p0, cudaStream_t stream, bool
   GemmParams<float> p;
   int am = 0, bm = 0;
   if (!orient(p0, &p, &am, &bm)) return 0;
-  if (!forced && (p.m < 64 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
+  // M >= 32: a 32-row problem pads the 128-row tile 4x, but the many-batch
+  // shapes that reach here (Tucker products with a rank-32 mode first) are
+  // HBM-bound, where the padding costs nothing and the SIMT fallback does
+  if (!forced && (p.m < 32 || p.n < 8 || double(p.m) * p.n * p.k * p.batch * p.batch2 < 2e6))
     return 0;
   int bn = env_int("SBT_TC_BN", 0);
   if (bn != 32 && bn != 64 && bn != 128 && bn != 256)

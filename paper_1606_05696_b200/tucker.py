@@ -191,6 +191,24 @@ def _sign_fix(u):
     return u * signs
 
 
+def _unfolding64(t: DenseTensor, r: int):
+    """fp64 buffer holding the mode-r unfolding Y_(r) column-major with leading
+    dimension dims[r] (mode r first), and its (rows, cols).  An fp64 packed
+    tensor is used in place for r = 0; otherwise one fused pass converts to
+    fp64 and moves mode r first."""
+    torch = _torch()
+    dims = t.layout.dims
+    rows = dims[r]
+    cols = int(np.prod(dims)) // rows
+    if r == 0 and t.dtype == torch.float64 and t.layout.is_packed():
+        return t.data, rows, cols
+    x = t.view().movedim(r, 0)                       # logical (rows, rest...)
+    rev = tuple(reversed(range(x.dim())))
+    buf = torch.empty(tuple(x.shape[i] for i in rev), dtype=torch.float64, device=t.device)
+    buf.copy_(x.permute(rev))                         # column-major, mode r fastest
+    return buf.reshape(-1), rows, cols
+
+
 def gram_of_unfolding(t: DenseTensor, r: int):
     """fp64 Gram matrix Y_(r) Y_(r)^T of the mode-r unfolding, on the device.
 
@@ -255,6 +273,69 @@ def _factor_from_tensor(t: DenseTensor, r: int, rank: int, warm=None):
     tol = _SUBSPACE_TOL if t.dtype == torch.float64 else _SUBSPACE_TOL_F32
     _, vecs, _ = top_eigh(gram_of_unfolding(t, r), rank, q0=warm, tol=tol)
     return _sign_fix(vecs.contiguous())
+
+
+# Device-finished sweeps (k_ritz.cuh): inside HOOI, a warm-started factor
+# update normally converges in ONE subspace sweep (the previous factor spans
+# the new leading subspace to ~1e-8).  The sweep's projected eigenproblem,
+# Ritz vectors, residual test and sign rule then run in one kernel with no
+# host round trip; the convergence flags of all factors are read once per
+# iteration together with ||G||, and an iteration with an unconverged factor
+# is recomputed on the host-driven path (top_eigh: more sweeps, oversampling,
+# full eigh), so results are those of the host path either way.
+_RITZ_MAX_P = 64
+RITZ_LOG = None  # set to a list to collect each sweep's diagnostics (rel[0..4])
+
+
+def _ritz_eligible(n: int, rank: int, warm) -> bool:
+    return (warm is not None and getattr(warm, "is_cuda", False) and n >= _SUBSPACE_MIN_N
+            and 4 * rank <= n and rank <= _RITZ_MAX_P)
+
+
+def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
+                   sweeps: int = 1):
+    """Warm-started subspace sweeps on the mode-r Gram, each finished on the
+    device (``sbt_ritz_f64``): sweep 1 on the previous factor, further sweeps
+    on the orthonormalised G U (one sweep reaches the fp32 tolerance after the
+    first HOOI iteration; fp64's 1e-12 takes two).  Writes the last sweep's
+    convergence flag to status[slot]; never synchronises."""
+    import ctypes
+    from . import _lib
+    torch = _torch()
+    fp64 = t.dtype == torch.float64
+    tol = _SUBSPACE_TOL if fp64 else _SUBSPACE_TOL_F32
+    # G Q = Y (Y^T Q) from the fp64 unfolding: two rank-p products instead of
+    # the n x n Gram (n^2 * cols flops) and G Q
+    y, n, cols = _unfolding64(t, r)
+    dev = y.device
+    wbuf = torch.empty(rank, cols, device=dev, dtype=torch.float64)  # Y^T Q, col-major
+    lib = _lib.load()
+    ptr = ctypes.c_void_p
+    stream = ptr(torch.cuda.current_stream(dev).cuda_stream)
+    qt = torch.as_tensor(warm, device=dev).t()
+    p = rank
+    for sweep in range(sweeps):
+        qz = torch.empty(2 * p, n, device=dev, dtype=torch.float64)   # [Q | Z] col-major
+        qz[:p].copy_(qt)
+        _gemm64(Op.Transpose, Op.Normal, cols, p, n, y, n, qz[:p], n, wbuf, cols)  # Y^T Q
+        _gemm64(Op.Normal, Op.Normal, n, p, cols, y, n, wbuf, cols, qz[p:], n)     # Z = Y (Y^T Q)
+        m = torch.empty(p, 2 * p, device=dev, dtype=torch.float64)
+        _gemm64(Op.Transpose, Op.Normal, 2 * p, p, n, qz, n, qz[p:], n, m, 2 * p)  # [Q Z]^T Z
+        last = sweep == sweeps - 1
+        ut = torch.empty(rank, n, device=dev, dtype=torch.float64)
+        yt = None if last else torch.empty(rank, n, device=dev, dtype=torch.float64)
+        w = torch.empty(rank, device=dev, dtype=torch.float64)
+        rel = torch.empty(6, device=dev, dtype=torch.float64)
+        flag = status[slot:] if last else torch.empty(1, device=dev, dtype=torch.int32)
+        _lib.check(lib.sbt_ritz_f64(
+            ptr(qz.data_ptr()), ptr(m.data_ptr()), n, p, rank, float(tol), ptr(ut.data_ptr()),
+            ptr(yt.data_ptr() if yt is not None else None), ptr(w.data_ptr()),
+            ptr(flag.data_ptr()), ptr(rel.data_ptr()), stream), "sbt_ritz_f64")
+        if RITZ_LOG is not None:
+            RITZ_LOG.append(rel)              # device tensors: diagnostics only
+        if not last:
+            qt = _orthonormal(yt)
+    return ut.t()
 
 
 def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
@@ -337,14 +418,98 @@ def _reuses_mode0(t: DenseTensor) -> bool:
     return t.layout.order == 3 and d[0] >= d[2] and d[0] >= d[1]
 
 
+def _hooi_sweep(t: DenseTensor, factors, fast: bool, factor_fn) -> DenseTensor:
+    """One HOOI iteration (tucker.py:160-167): update every factor in place via
+    factor_fn(y, r, warm) and return the core G = T x_1 U_1^T ... x_N U_N^T."""
+    order = t.layout.order
+    if fast:
+        # skip=0 chain: modes 1, 2 (reference order); then X0 = T x_0 U_0^T
+        y = _mode_product_chain(t, factors, skip=0, transpose=True)
+        factors[0] = factor_fn(y, 0, factors[0])
+        x0 = _mode_product(t, factors[0], 0, True)
+        # reference skip=1 chain is [0, 2] and skip=2 chain is [0, 1]
+        y = _mode_product(x0, factors[2], 2, True)
+        factors[1] = factor_fn(y, 1, factors[1])
+        y2 = _mode_product(x0, factors[1], 1, True)
+        factors[2] = factor_fn(y2, 2, factors[2])
+        # reference core chain: mode 0, then the larger of modes 1 / 2 first
+        if t.layout.dims[1] >= t.layout.dims[2]:
+            return _mode_product(y2, factors[2], 2, True)
+        return _mode_product(_mode_product(x0, factors[2], 2, True), factors[1], 1, True)
+    for r in range(order):
+        y = _mode_product_chain(t, factors, skip=r, transpose=True)
+        factors[r] = factor_fn(y, r, factors[r])
+    return tucker_core(t, factors)
+
+
+class _IterationGraph:
+    """One device-finished HOOI iteration captured as a CUDA graph (the
+    iteration is launch-only, so after the first capture a replay costs no
+    host work).  Static buffers: ``factors`` (read as the warm start, then
+    overwritten with the iteration's new factors), ``saved`` (the factors the
+    iteration started from, for the host-path redo) and ``out`` = [||G||,
+    convergence flags...]."""
+
+    @classmethod
+    def capture(cls, t, factors, ranks, fast, sweeps):
+        torch = _torch()
+        self = cls()
+        order = t.layout.order
+        self.factors = [f.contiguous().clone() for f in factors]
+        self.saved = [torch.empty_like(f) for f in self.factors]
+        self.status = torch.zeros(order, dtype=torch.int32, device=t.device)
+        self.graph = torch.cuda.CUDAGraph()
+        # capture_begin/end on a side stream directly: torch.cuda.graph() would
+        # also gc.collect() and empty the caching allocator on every capture
+        side = torch.cuda.Stream(device=t.device)
+        side.wait_stream(torch.cuda.current_stream(t.device))
+        try:
+            with torch.cuda.stream(side):
+                self.graph.capture_begin()
+                try:
+                    self._record(t, ranks, fast, sweeps)
+                finally:
+                    self.graph.capture_end()
+        except RuntimeError:      # something on the path is not capturable
+            torch.cuda.synchronize()
+            return None
+        torch.cuda.current_stream(t.device).wait_stream(side)
+        return self
+
+    def _record(self, t, ranks, fast, sweeps):
+        torch = _torch()
+        for sv, f in zip(self.saved, self.factors):
+            sv.copy_(f)
+        self.status.zero_()
+        work = list(self.factors)
+        core = _hooi_sweep(t, work, fast, lambda y, r, warm: _factor_device(
+            y, r, ranks[r], warm, self.status, r, sweeps))
+        norm_g = torch.linalg.vector_norm(core.data.to(torch.float64)).reshape(1)
+        self.out = torch.cat([norm_g, self.status.to(torch.float64)])
+        for f, u in zip(self.factors, work):
+            f.copy_(u)
+
+    def replay(self):
+        self.graph.replay()
+        return self.out.cpu().numpy()
+
+    def restore(self):
+        for f, sv in zip(self.factors, self.saved):
+            f.copy_(sv)
+
+
 def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
-         reuse_mode0: bool = True) -> TuckerModel:
+         reuse_mode0: bool = True, device_ritz: bool = True,
+         use_graph: bool = True) -> TuckerModel:
     """Higher-order orthogonal iteration (reference tucker.py:136-174).
 
     With ``reuse_mode0`` (order-3 tensors whose mode 0 is the largest) the
     product T x_0 U_0^T that the reference recomputes three times per iteration
     is computed once: T is read twice per iteration instead of four times, with
-    the same operations in the same order."""
+    the same operations in the same order.  With ``device_ritz`` the warm
+    factor updates finish on the device (see _factor_device) and an iteration
+    synchronises with the host once; with ``use_graph`` that iteration is
+    captured once as a CUDA graph and replayed (long runs only)."""
     order = t.layout.order
     ranks = tuple(int(r) for r in ranks)
     if len(ranks) != order:
@@ -359,34 +524,48 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
     prev = -np.inf
     iters = 0
     fast = reuse_mode0 and _reuses_mode0(t)
+    host_factor = lambda y, r, warm: _factor_from_tensor(y, r, ranks[r], warm=warm)  # noqa: E731
+    graph = None
     for it in range(max_iters):
         iters = it + 1
-        if fast:
-            # skip=0 chain: modes 1, 2 (reference order); then X0 = T x_0 U_0^T
-            y = _mode_product_chain(t, factors, skip=0, transpose=True)
-            factors[0] = _factor_from_tensor(y, 0, ranks[0], warm=factors[0])
-            x0 = _mode_product(t, factors[0], 0, True)
-            # reference skip=1 chain is [0, 2] and skip=2 chain is [0, 1]
-            y = _mode_product(x0, factors[2], 2, True)
-            factors[1] = _factor_from_tensor(y, 1, ranks[1], warm=factors[1])
-            y2 = _mode_product(x0, factors[1], 1, True)
-            factors[2] = _factor_from_tensor(y2, 2, ranks[2], warm=factors[2])
-            # reference core chain: mode 0, then the larger of modes 1 / 2 first
-            if t.layout.dims[1] >= t.layout.dims[2]:
-                core = _mode_product(y2, factors[2], 2, True)
+        if device_ritz and all(_ritz_eligible(t.layout.dims[r], ranks[r], factors[r])
+                               for r in range(order)):
+            sweeps = 2 if (it == 0 or t.dtype == torch.float64) else 1
+            if graph is None and use_graph and it >= 1 and max_iters - it >= 3:
+                graph = _IterationGraph.capture(t, factors, ranks, fast, sweeps)
+                if graph is not None:
+                    factors = graph.factors
+            if graph is not None:
+                vals = graph.replay()                # one sync
             else:
-                core = _mode_product(_mode_product(x0, factors[2], 2, True), factors[1], 1, True)
+                saved = list(factors)
+                status = torch.zeros(order, dtype=torch.int32, device=t.device)
+                core = _hooi_sweep(t, factors, fast, lambda y, r, warm: _factor_device(
+                    y, r, ranks[r], warm, status, r, sweeps))
+                norm_g2 = torch.linalg.vector_norm(core.data.to(torch.float64)).reshape(1)
+                vals = torch.cat([norm_g2, status.to(torch.float64)]).cpu().numpy()  # one sync
+            if np.all(vals[1:] == 1.0):
+                norm_g = float(vals[0])
+            else:                                    # an unconverged factor: host path
+                if graph is not None:
+                    graph.restore()
+                    work = [f.clone() for f in factors]
+                    core = _hooi_sweep(t, work, fast, host_factor)
+                    for f, u in zip(factors, work):
+                        f.copy_(u)
+                else:
+                    factors[:] = saved
+                    core = _hooi_sweep(t, factors, fast, host_factor)
+                norm_g = _norm(core)
         else:
-            for r in range(order):
-                y = _mode_product_chain(t, factors, skip=r, transpose=True)
-                factors[r] = _factor_from_tensor(y, r, ranks[r], warm=factors[r])
-            core = tucker_core(t, factors)
-        norm_g = _norm(core)
+            core = _hooi_sweep(t, factors, fast, host_factor)
+            norm_g = _norm(core)
         resid = np.sqrt(max(0.0, norm_t ** 2 - norm_g ** 2))
         fit = 1.0 - resid / norm_t if norm_t > 0 else 1.0
         fits.append(fit)
         if fit - prev < tol and it > 0:
             break
         prev = fit
+    factors = [f.contiguous() for f in factors]
     core = tucker_core(t, factors)
     return TuckerModel(core=core, factors=factors, fit_history=fits, iterations=iters)

@@ -607,6 +607,105 @@ def test_hooi_subspace_path_matches_oracle():
             np.testing.assert_allclose(u, ur, atol=utol)
 
 
+def _gapped_gram(rng, n, r, cols=600):
+    x = rng.standard_normal((n, r)) @ np.diag(np.linspace(10, 3, r)) @ rng.standard_normal((r, cols))
+    x += 1e-3 * rng.standard_normal((n, cols))
+    return x @ x.T
+
+
+@pytest.mark.parametrize("n,rank", [(256, 16), (512, 32), (200, 13), (384, 48)])
+def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank):
+    """sbt_ritz_f64 (device Jacobi + Ritz vectors + residual test + sign rule)
+    equals the host Rayleigh-Ritz step of top_eigh on the same sweep."""
+    import ctypes
+    from paper_1606_05696_b200 import _lib
+    rng = np.random.default_rng(n + rank)
+    g = _gapped_gram(rng, n, rank + 4)
+    wr, vr = np.linalg.eigh(g)
+    wr, vr = wr[::-1], vr[:, ::-1]
+    # warm basis: exact leading vectors, slightly perturbed, orthonormalised
+    q = np.linalg.qr(vr[:, :rank] + 1e-4 * rng.standard_normal((n, rank)))[0]
+    qz = np.concatenate([q.T, (g @ q).T])                 # [Q | Z] as rows
+    m = qz @ (g @ q)                                      # [Q Z]^T Z, (2p, p)
+    dq = torch.as_tensor(qz, device="cuda").contiguous()
+    dm = torch.as_tensor(np.asfortranarray(m).ravel(order="F"), device="cuda")
+    ut = torch.empty(rank, n, dtype=torch.float64, device="cuda")
+    yt = torch.empty_like(ut)
+    w = torch.empty(rank, dtype=torch.float64, device="cuda")
+    flag = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    rel = torch.empty(6, dtype=torch.float64, device="cuda")
+    P = ctypes.c_void_p
+    _lib.check(_lib.load().sbt_ritz_f64(
+        P(dq.data_ptr()), P(dm.data_ptr()), n, rank, rank, 1e-12, P(ut.data_ptr()),
+        P(yt.data_ptr()), P(w.data_ptr()), P(flag.data_ptr()), P(rel.data_ptr()), P(0)),
+        "ritz")
+    torch.cuda.synchronize()
+    h = m[:rank]
+    hw, hv = np.linalg.eigh(0.5 * (h + h.T))
+    hw, hv = hw[::-1], hv[:, ::-1]
+    np.testing.assert_allclose(w.cpu().numpy(), hw, rtol=1e-12)
+    u = q @ hv
+    u = u * np.where(u[np.argmax(np.abs(u), axis=0), np.arange(rank)] < 0, -1.0, 1.0)
+    np.testing.assert_allclose(ut.cpu().numpy().T, u, atol=1e-10)
+    r = np.linalg.norm(g @ u - u * hw, axis=0).max() / hw[0]
+    assert abs(rel[0].item() - r) <= 1e-6 * r + 1e-15
+    # nearly diagonal H: Newton refinement steps, few or no Jacobi sweeps
+    assert 1 <= rel[5].item() + rel[1].item() and rel[1].item() <= 6
+    assert flag.item() == int(r <= 1e-12)
+    # Y = G U before the sign rule: |Y| columns match G u
+    np.testing.assert_allclose(np.abs(yt.cpu().numpy().T), np.abs(g @ u), atol=1e-8 * hw[0])
+
+
+def test_hooi_device_ritz_equals_host_path():
+    """HOOI with the device-finished sweeps (one host sync per iteration)
+    gives the host-driven path's fits and factors, fp32 and fp64."""
+    rng = np.random.default_rng(21)
+    dims, ranks = (256, 192, 160), (16, 12, 8)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    for dtype, ftol, utol in (("float64", 1e-12, 1e-9), ("float32", 1e-6, 1e-5)):
+        t = DenseTensor.from_array(full, dtype=dtype)
+        m1 = sbt.hooi(t, ranks, max_iters=4, tol=-1.0, device_ritz=True)
+        m2 = sbt.hooi(t, ranks, max_iters=4, tol=-1.0, device_ritz=False)
+        np.testing.assert_allclose(m1.fit_history, m2.fit_history, rtol=0, atol=ftol)
+        for u1, u2 in zip(m1.factors, m2.factors):
+            np.testing.assert_allclose(u1.cpu().numpy(), u2.cpu().numpy(), atol=utol)
+
+
+def test_hooi_graph_replay_equals_eager():
+    """The CUDA-graph replay of the device-finished iteration gives bitwise
+    the eager iteration's fits and factors (same kernels, same order)."""
+    rng = np.random.default_rng(22)
+    dims, ranks = (256, 160, 192), (16, 8, 12)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    for dtype in ("float32", "float64"):
+        t = DenseTensor.from_array(full, dtype=dtype)
+        m1 = sbt.hooi(t, ranks, max_iters=6, tol=-1.0, use_graph=True)
+        m2 = sbt.hooi(t, ranks, max_iters=6, tol=-1.0, use_graph=False)
+        assert m1.fit_history == m2.fit_history
+        for u1, u2 in zip(m1.factors, m2.factors):
+            assert torch.equal(u1, u2)
+
+
+def test_device_ritz_flags_unconverged_sweep():
+    """A poor warm start does not converge in one sweep: the flag is 0 (HOOI
+    then recomputes the iteration on the host path)."""
+    from paper_1606_05696_b200 import tucker as tk
+    rng = np.random.default_rng(3)
+    n, rank = 256, 16
+    x = rng.standard_normal((n, 4000))
+    t = DenseTensor.from_array(x.reshape(n, 40, 100), dtype="float64")
+    warm = torch.linalg.qr(torch.randn(n, rank, dtype=torch.float64, device="cuda"))[0]
+    status = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    u = tk._factor_device(t, 0, rank, warm, status, 0)
+    torch.cuda.synchronize()
+    assert status.item() == 0
+    assert u.shape == (n, rank)
+
+
 @pytest.mark.parametrize("m,n,k,P", [(256, 256, 8192, 2), (128, 128, 40000, 1), (512, 320, 3000, 3)])
 def test_fp32_long_reductions_stay_within_tolerance(m, n, k, P):
     """3xTF32 truncation bias grows with K; long reductions are K-chunked (and
@@ -660,6 +759,10 @@ def test_fourth_order_n128_folds_both_batch_modes():
     (384, 256, 96, 5, "a", 0),
     (256, 384, 200, 3, 0, "b"),
     (640, 256, 64, 4, "a", 0),
+    # fewer than 128 rows per batch entry (MN-major A: 32-row boxes per entry)
+    (32, 32, 512, 512, "a", 0),
+    (96, 32, 200, 200, "a", 0),
+    (160, 64, 72, 64, "a", 0),
 ])
 def test_batch_fold_into_m_or_n(shape):
     m, n, k, P, aps, bps = shape

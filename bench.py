@@ -598,20 +598,29 @@ def run_config(args):
         sbt.hooi(t, (r, r, r), max_iters=1, tol=-1.0)  # warm-up: plans, libraries
         iters = max(2, args.steps)
 
+        import gc
+
         def run(k):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            m = sbt.hooi(t, (r, r, r), max_iters=k, tol=-1.0)
-            torch.cuda.synchronize()
-            return time.perf_counter() - t0, m
+            # Python's cyclic GC (20-30 ms gen-2 passes in this process) would
+            # land at random inside timed runs: collect first, pause it inside
+            gc.collect()
+            gc.disable()
+            try:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                m = sbt.hooi(t, (r, r, r), max_iters=k, tol=-1.0)
+                torch.cuda.synchronize()
+                return time.perf_counter() - t0, m
+            finally:
+                gc.enable()
 
         # steady-state cost per iteration = difference of a (1+K)- and a
         # (1+2K)-iteration run (both include the HOSVD init, the one-time
-        # capture of the iteration graph and the final core); best of 2 each.
+        # capture of the iteration graph and the final core); best of 3 each.
         # The 1-iteration run gives the per-iteration cost including capture.
-        t_init = min(run(1)[0] for _ in range(2))
-        t_k = min(run(1 + iters)[0] for _ in range(2))
-        runs = [run(1 + 2 * iters) for _ in range(2)]
+        t_init = min(run(1)[0] for _ in range(3))
+        t_k = min(run(1 + iters)[0] for _ in range(3))
+        runs = [run(1 + 2 * iters) for _ in range(3)]
         total, model = min(runs, key=lambda x: x[0])
         per_iter = (total - t_k) / iters
         per_iter_first_k = (t_k - t_init) / iters
@@ -624,6 +633,7 @@ def run_config(args):
                            "init_plus_one_iter_ms": round(t_init * 1e3, 1),
                            "ms_per_iter_incl_graph_capture": round(per_iter_first_k * 1e3, 3),
                            "iters_timed": iters,
+                           "hooi_paths": model.stats,
                            "contraction_gflop_per_iter": round(fl / 1e9, 2),
                            "fit_history": [round(f, 8) for f in model.fit_history]}}
     elif args.config == "conventional":

@@ -62,16 +62,19 @@ int sbt_probe_tf32_sustained(double seconds, double* tflops);
 /* ---- reference: tucker.py:63-76 leading_left_singular_vectors (the HOOI
         factor update).  Finishes one warm-started subspace sweep on the
         device: qz = [Q | Z] (2p rows of n doubles: the columns of Q, then of
-        Z = G Q), m = [Q Z]^T Z (2p x p column-major).  Writes the leading
+        Z = G Q), m = [Q Z]^T Z (2p x p column-major) or NULL (Q^T Z is then
+        formed in-kernel).  Writes the leading
         `rank` Ritz vectors, sign-fixed as tucker.py:71-75, to ut (rank rows of
         n) and, when yt is not NULL, Y = G U to yt (same shape, unsigned: the
-        next sweep's basis), their values (descending) to w, flag[0] = 1 when every residual
+        next sweep's basis), when ut32 is not NULL the sign-fixed vectors
+        rounded to fp32 (same shape), their values (descending) to w, flag[0] = 1 when every residual
         ||G u - w u|| <= tol * w_max, rel[0] = max residual / w_max, rel[1] = the
         number of Jacobi sweeps, rel[2..4] phase cycle counts, rel[5] Newton refinement steps (6
         doubles).  One
         kernel, no host synchronisation; p <= 64. */
 int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, double tol,
-                 double* ut, double* yt, double* w, int* flag, double* rel, void* stream);
+                 double* ut, double* yt, float* ut32, double* w, int* flag, double* rel,
+                 void* stream);
 
 /* ---- reference: layout.py:202-215 permute_copy (the conventional strategy's
         explicit transposition, planner.py:620-713; NOT used by planned

@@ -67,7 +67,7 @@ SIGNATURES = {
                         c_int),
     "sbt_permute_f32": ([c_int, ctypes.POINTER(c_int64), _P, ctypes.POINTER(c_int64), _P, _P],
                         c_int),
-    "sbt_ritz_f64": ([_P, _P, c_int64, c_int, c_int, c_double, _P, _P, _P, _P, _P, _P],
+    "sbt_ritz_f64": ([_P, _P, c_int64, c_int, c_int, c_double, _P, _P, _P, _P, _P, _P, _P],
                      c_int),
     "sbt_batched_core_group_f32": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),
     "sbt_batched_core_group_f64": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),

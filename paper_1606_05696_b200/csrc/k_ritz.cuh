@@ -39,8 +39,10 @@ constexpr int kThreads = 512;
 constexpr int kCluster = 8;                    // CTAs sharing the Ritz-vector phase
 constexpr int LDS = kMaxP + 1;
 constexpr int MAT = kMaxP * LDS;               // one P x P matrix (padded rows)
-constexpr int kTileRows = 64;                  // Ritz-vector phase row tile
-constexpr int REGION0 = (5 * MAT > 2 * kTileRows * kMaxP) ? 5 * MAT : 2 * kTileRows * kMaxP;
+constexpr int kTileRows = 64;                  // Q / Z row tile
+constexpr int LDT = kTileRows + 1;             // tile row stride (conflict-free column walks)
+constexpr int REGION0 = 5 * MAT;  // >= the two Q / Z tiles (2 * kMaxP * LDT)
+static_assert(2 * kMaxP * LDT <= 4 * MAT, "Q / Z tiles must leave slot 4 free");
 constexpr int kTri = kHalf * (kHalf + 1) / 2;  // upper-triangular 2 x 2 blocks
 constexpr int SMEM_BYTES =
     (REGION0 + 4 * kMaxP) * 8 + (2 * kMaxP) * 4 + (kMaxP * kMaxP + 2 * kTri) + 64;
@@ -78,15 +80,18 @@ __device__ __forceinline__ void small_mm(const double* X, const double* Y, doubl
 
 // qz: [Q | Z] stored as 2p rows of length n (row j = column j of Q, then of Z);
 // m: the (2p x p) column-major product [Q Z]^T Z (ld 2p).
+// m == nullptr: H = Q^T Z is formed in-kernel.
 // ut: rank rows of length n (U column-major); yt (optional): the same for
-// Y = G U (the next sweep's basis, before the sign rule); w: rank eigenvalues
+// Y = G U (the next sweep's basis, before the sign rule); ut32 (optional): U
+// rounded to fp32; w: rank eigenvalues
 // (descending); flag[0] = converged; rel[0] = max residual / w_max,
 // rel[1] = Jacobi sweeps, rel[2..4] = SM cycles of the eigen / Ritz-vector /
 // sign phases, rel[5] = Newton refinement steps (diagnostics).
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
 ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t n, int p,
             int rank, double tol, double* __restrict__ ut, double* __restrict__ yt,
-            double* __restrict__ w, int* __restrict__ flag, double* __restrict__ rel) {
+            float* __restrict__ ut32, double* __restrict__ w, int* __restrict__ flag,
+            double* __restrict__ rel) {
   extern __shared__ __align__(16) double smr[];
   // eigen phase: A double-buffered at smr + {0, 1} * MAT (buffer 1 is W in the
   // Newton phase), V at smr + 2 * MAT, H at smr + 3 * MAT, S at smr + 4 * MAT
@@ -94,8 +99,8 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
   double* H = smr + 3 * MAT;
   double* S = smr + 4 * MAT;
   double* W = smr + MAT;
-  double* Qs = smr;                     // [p][kTileRows] (Ritz phase, reuses A / V)
-  double* Zs = smr + kTileRows * kMaxP;
+  double* Qs = smr;                     // [p][LDT] row tiles (reuse A / V)
+  double* Zs = smr + kMaxP * LDT;
   double* Vs = smr + 4 * MAT;           // [p][LDS]: sorted leading eigenvectors (reuses S)
   double* wv = smr + REGION0;           // sorted eigenvalues
   double* res = wv + kMaxP;             // [rank] squared residuals
@@ -120,6 +125,61 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
   const int crank = int(cluster.block_rank());
   int sweeps = 0, newton = 0;
   long long t_jacobi = t_start;
+  // stage rows [i0, i0 + rows) of Q and Z into Qs / Zs ([l][LDT], row fastest)
+  auto load_tile = [&](int64_t i0, int rows) {
+    for (int e = tid; e < p * kTileRows; e += kThreads) {
+      const int l = e / kTileRows, rr = e % kTileRows;
+      const bool in = rr < rows;
+      Qs[l * LDT + rr] = in ? qz[int64_t(l) * n + i0 + rr] : 0.0;
+      Zs[l * LDT + rr] = in ? qz[int64_t(p + l) * n + i0 + rr] : 0.0;
+    }
+  };
+  // m == nullptr: H = Q^T Z from the cluster's row tiles (partial per CTA in
+  // slot 4, summed in CTA order by CTA 0) instead of a separate GEMM
+  double* Hp = smr + 4 * MAT;
+  if (m == nullptr) {
+    double hacc[kMaxP * kMaxP / kThreads];
+#pragma unroll
+    for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) hacc[t] = 0.0;
+    for (int64_t i0 = int64_t(crank) * kTileRows; i0 < n; i0 += kCluster * kTileRows) {
+      const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
+      load_tile(i0, rows);
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) {
+        const int e = tid + t * kThreads;
+        if (e >= p * p) break;
+        const int i = e / p, j = e % p;
+        const double* qi = Qs + i * LDT;
+        const double* zj = Zs + j * LDT;
+        double a = hacc[t];
+        for (int r = 0; r < kTileRows; ++r) a = fma(qi[r], zj[r], a);
+        hacc[t] = a;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) {
+      const int e = tid + t * kThreads;
+      if (e < p * p) Hp[(e / p) * LDS + e % p] = hacc[t];
+    }
+    cluster.sync();
+    // each CTA sums a slice of the entries over the cluster (CTA order, the
+    // eight remote loads in flight together) into CTA 0's slot 3
+    double* H0 = cluster.map_shared_rank(smr + 3 * MAT, 0);
+    const int per = (p * p + kCluster - 1) / kCluster;
+    for (int e = crank * per + tid; e < (crank + 1) * per && e < p * p; e += kThreads) {
+      const int off = (e / p) * LDS + e % p;
+      double v[kCluster];
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) v[c] = *cluster.map_shared_rank(Hp + off, c);
+      double sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) sum += v[c];
+      H0[off] = sum;
+    }
+    cluster.sync();
+  }
   if (crank == 0) {  // the eigen phase runs on CTA 0; the others wait
     // round-robin schedule (circle method: position 0 holds player P-1) and
     // the upper-triangular block list
@@ -142,14 +202,24 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
     for (int e = tid; e < P * P; e += kThreads) {
       const int i = e / P, j = e % P;
       double h = 0.0;
-      if (i < p && j < p) h = 0.5 * (m[i + j * ldm] + m[j + i * ldm]);
+      if (i < p && j < p) {
+        if (m) {
+          h = 0.5 * (m[i + j * ldm] + m[j + i * ldm]);
+        } else {  // the cluster-summed Q^T Z (slot 3, read before H is written)
+          h = 0.5 * (H[i * LDS + j] + H[j * LDS + i]);
+        }
+      }
       smr[i * LDS + j] = h;
-      H[i * LDS + j] = h;
       V[i * LDS + j] = i == j ? 1.0 : 0.0;
       fro += h * h;
     }
     for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
     if ((tid & 31) == 0) atomicAdd(&s_red[0], fro);
+    __syncthreads();
+    for (int e = tid; e < P * P; e += kThreads) {  // H keeps the symmetrised start
+      const int i = e / P, j = e % P;
+      H[i * LDS + j] = smr[i * LDS + j];
+    }
     __syncthreads();
     // rotate only while |a_pq| > floor: the residual test is relative to w_max,
     // so off-diagonal mass far below tol * ||H|| changes no decision (a test
@@ -357,8 +427,6 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
 
   // U = Q V_r, Y = Z V_r over row tiles (tile t on CTA t % kCluster);
   // thread = (row r, 8-column group g)
-  const double* Q = qz;
-  const double* Z = qz + int64_t(p) * n;
   const int r = tid % kTileRows, g = tid / kTileRows;  // 8 groups of 8 columns
   const int ngroups = (rank + 7) / 8;
   double rsum[8], mx[8];
@@ -367,12 +435,7 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
   for (int jj = 0; jj < 8; ++jj) rsum[jj] = 0.0, mx[jj] = -1.0, ax[jj] = 0x7fffffff;
   for (int64_t i0 = int64_t(crank) * kTileRows; i0 < n; i0 += kCluster * kTileRows) {
     const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
-    for (int e = tid; e < p * kTileRows; e += kThreads) {
-      const int l = e / kTileRows, rr = e % kTileRows;
-      const bool in = rr < rows;
-      Qs[l * kTileRows + rr] = in ? Q[int64_t(l) * n + i0 + rr] : 0.0;
-      Zs[l * kTileRows + rr] = in ? Z[int64_t(l) * n + i0 + rr] : 0.0;
-    }
+    load_tile(i0, rows);
     __syncthreads();
     if (g < ngroups) {
       const int j0 = 8 * g;
@@ -380,7 +443,7 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) u[jj] = y[jj] = 0.0;
       for (int l = 0; l < p; ++l) {
-        const double q = Qs[l * kTileRows + r], z = Zs[l * kTileRows + r];
+        const double q = Qs[l * LDT + r], z = Zs[l * LDT + r];
         const double* vr = Vs + l * LDS + j0;
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
@@ -459,7 +522,10 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
     const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
     for (int e = tid; e < rank * kTileRows; e += kThreads) {
       const int j = e / kTileRows, rr = e % kTileRows;
-      if (rr < rows && sgn[j] < 0.0) ut[int64_t(j) * n + i0 + rr] *= -1.0;
+      if (rr >= rows) continue;
+      double* u = ut + int64_t(j) * n + i0 + rr;
+      if (sgn[j] < 0.0) *u = -*u;
+      if (ut32) ut32[int64_t(j) * n + i0 + rr] = float(*u);
     }
   }
   if (crank == 0 && tid < 32) {  // one warp: residual norms and the flag

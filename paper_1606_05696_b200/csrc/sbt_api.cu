@@ -452,8 +452,9 @@ SBT_DEFINE(float, f32)
 // update, reference tucker.py:63-76); see k_ritz.cuh.  Asynchronous: the
 // convergence flag is read by the caller later.
 int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, double tol,
-                 double* ut, double* yt, double* w, int* flag, double* rel, void* stream) {
-  if (!qz || !m || !ut || !w || !flag || !rel || n < 1 || p < 1 || p > ritz::kMaxP ||
+                 double* ut, double* yt, float* ut32, double* w, int* flag, double* rel,
+                 void* stream) {
+  if (!qz || !ut || !w || !flag || !rel || n < 1 || p < 1 || p > ritz::kMaxP ||
       rank < 1 || rank > p || p > n)
     return fail(SBT_EINVAL, "sbt_ritz_f64: bad arguments");
   static bool attr = false;
@@ -466,7 +467,7 @@ int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, 
     attr = true;
   }
   ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-      qz, m, n, p, rank, tol, ut, yt, w, flag, rel);
+      qz, m, n, p, rank, tol, ut, yt, ut32, w, flag, rel);
   note_launch("ritz");
   return check_cuda(cudaGetLastError(), "ritz launch");
 }

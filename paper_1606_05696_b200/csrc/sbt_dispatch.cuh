@@ -15,6 +15,7 @@
 
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
+#include "k_skinny_dmma.cuh"
 #include "k_tf32x3.cuh"
 #include "k_tf32x3_pair_tma.cuh"
 #include "k_dmma.cuh"
@@ -737,8 +738,85 @@ static int launch_chunked(const GemmParams<T>& p, cudaStream_t stream) {
   return launch_gemm_core<T>(p, stream);
 }
 
+// fp64 skinny products (no batch, N <= 64 in one orientation, enough work to
+// matter): 64 x 32 DMMA tiles, in-kernel deterministic split-K (k_skinny_dmma).
+static void keep_pool_memory() {
+  static bool done = [] {  // keep freed workspaces in the stream-ordered pool
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return true;
+  }();
+  (void)done;
+}
+
+template <bool AK, bool BK_>
+static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
+  using namespace skinny;
+  auto kern = skinny_dmma_kernel<AK, BK_>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess)
+      return -3;
+    attr = true;
+  }
+  const int64_t tiles_m = ceil_div(p.m, BM), tiles = tiles_m * ceil_div(p.n, BN);
+  if (tiles > 65535 * 16) return 0;
+  // splits: fill ~2 waves of CTAs, at least 2 K-chunks (of KC) per split
+  int64_t S = (2 * kNumSMs + tiles - 1) / tiles;
+  const int64_t max_s = p.k / (2 * KC);
+  if (S > max_s) S = max_s;
+  if (S > 64) S = 64;
+  if (S < 1) S = 1;
+  const int64_t kper = ceil_div(ceil_div(p.k, S), KC) * KC;
+  S = ceil_div(p.k, kper);
+  double* ws = nullptr;
+  unsigned* cnt = nullptr;
+  if (S > 1) {
+    keep_pool_memory();
+    const size_t wbytes = size_t(tiles) * S * TILE * sizeof(double);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + tiles * sizeof(unsigned),
+                        stream) != cudaSuccess)
+      return -3;
+    cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + wbytes);
+    cudaMemsetAsync(cnt, 0, tiles * sizeof(unsigned), stream);
+  }
+  kern<<<dim3(unsigned(tiles), unsigned(S)), NT, SMEM_BYTES, stream>>>(p, int(tiles_m), kper, ws,
+                                                                       cnt);
+  note_launch("skinny_dmma_f64");
+  if (ws) cudaFreeAsync(ws, stream);
+  return 1;
+}
+
+static int try_skinny_f64(const GemmParams<double>& p0, cudaStream_t stream) {
+  static const int enabled = env_int("SBT_SKINNY", 1);
+  if (!enabled || p0.batch != 1 || p0.batch2 != 1 || p0.m == 1 || p0.n == 1) return 0;
+  // orientation with the narrow side as N
+  const GemmParams<double> p = (p0.n <= skinny::BN * 2 || p0.m > skinny::BN * 2) ? p0
+                                                                                  : transposed(p0);
+  if (p.n > 2 * skinny::BN || p.m < 16 || p.k < 32) return 0;
+  if (double(p.m) * p.n * p.k < 2e5) return 0;  // tiny: the generic kernel
+  const bool ak = p.acs == 1, amn = p.ars == 1;
+  const bool bk = p.brs == 1, bn = p.bcs == 1;
+  if (!(ak || amn) || !(bk || bn)) return 0;
+  if (ak && bk) return launch_skinny_cfg<true, true>(p, stream);
+  if (ak) return launch_skinny_cfg<true, false>(p, stream);
+  if (bk) return launch_skinny_cfg<false, true>(p, stream);
+  return launch_skinny_cfg<false, false>(p, stream);
+}
+
 template <typename T>
 static int launch_gemm(const GemmParams<T>& p, cudaStream_t stream) {
+  if constexpr (sizeof(T) == 8) {
+    if (kernel_override() == 0) {
+      const int rc = try_skinny_f64(p, stream);
+      if (rc != 0) return rc < 0 ? rc : 0;
+    }
+  }
   if (kernel_override() == 0) {
     const int rc = try_split_k<T>(p, stream);
     if (rc < 0) return rc;

@@ -413,7 +413,10 @@ def test_split_k_for_tall_reductions():
         c = torch.zeros(m * n, dtype=dtype, device="cuda")
         n0 = _lib.launch_count()
         kernels.gemm("N", "N", m, n, k, 1.0, a, m, b, k, 0.0, c, m)
-        assert _lib.launch_count() - n0 >= 2  # split partials + reduction
+        if dtype == torch.float64:   # narrow N: the skinny kernel reduces its splits in-kernel
+            assert _lib.last_kernel() == "skinny_dmma_f64", _lib.last_kernel()
+        else:
+            assert _lib.launch_count() - n0 >= 2  # split partials + reduction
         want = np.zeros(m * n)
         oapi.run_call("gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=1.0, lda=m, ldb=k,
                       beta=0.0, ldc=m), host(a), host(b), want)
@@ -456,7 +459,8 @@ def test_hooi_mode0_reuse_is_bitwise_identical():
 def test_tensor_paths_are_used_for_the_36_cases():
     """No silent fallback: at n=64 every case runs on a tensor-core kernel."""
     rng = np.random.default_rng(1)
-    for dtype, prefix in ((torch.float32, "tc_tf32x3"), (torch.float64, "tc_dmma")):
+    for dtype, prefix in ((torch.float32, ("tc_tf32x3",)),
+                          (torch.float64, ("tc_dmma", "skinny_dmma"))):
         for case in enumerate_cases(2, 3):
             spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
             la, lb, lc = _packed(spec, dict(m=64, n=64, p=64, k=64))
@@ -613,8 +617,9 @@ def _gapped_gram(rng, n, r, cols=600):
     return x @ x.T
 
 
-@pytest.mark.parametrize("n,rank", [(256, 16), (512, 32), (200, 13), (384, 48)])
-def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank):
+@pytest.mark.parametrize("n,rank,fused", [(256, 16, 0), (512, 32, 0), (200, 13, 1), (384, 48, 1),
+                                          (512, 32, 1), (1000, 64, 1)])
+def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank, fused):
     """sbt_ritz_f64 (device Jacobi + Ritz vectors + residual test + sign rule)
     equals the host Rayleigh-Ritz step of top_eigh on the same sweep."""
     import ctypes
@@ -631,14 +636,15 @@ def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank):
     dm = torch.as_tensor(np.asfortranarray(m).ravel(order="F"), device="cuda")
     ut = torch.empty(rank, n, dtype=torch.float64, device="cuda")
     yt = torch.empty_like(ut)
+    u32 = torch.empty(rank, n, dtype=torch.float32, device="cuda")
     w = torch.empty(rank, dtype=torch.float64, device="cuda")
     flag = torch.full((1,), -1, dtype=torch.int32, device="cuda")
     rel = torch.empty(6, dtype=torch.float64, device="cuda")
     P = ctypes.c_void_p
     _lib.check(_lib.load().sbt_ritz_f64(
-        P(dq.data_ptr()), P(dm.data_ptr()), n, rank, rank, 1e-12, P(ut.data_ptr()),
-        P(yt.data_ptr()), P(w.data_ptr()), P(flag.data_ptr()), P(rel.data_ptr()), P(0)),
-        "ritz")
+        P(dq.data_ptr()), P(dm.data_ptr()) if fused == 0 else None, n, rank, rank, 1e-12,
+        P(ut.data_ptr()), P(yt.data_ptr()), P(u32.data_ptr()), P(w.data_ptr()),
+        P(flag.data_ptr()), P(rel.data_ptr()), P(0)), "ritz")
     torch.cuda.synchronize()
     h = m[:rank]
     hw, hv = np.linalg.eigh(0.5 * (h + h.T))
@@ -647,6 +653,7 @@ def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank):
     u = q @ hv
     u = u * np.where(u[np.argmax(np.abs(u), axis=0), np.arange(rank)] < 0, -1.0, 1.0)
     np.testing.assert_allclose(ut.cpu().numpy().T, u, atol=1e-10)
+    assert torch.equal(u32, ut.to(torch.float32))
     r = np.linalg.norm(g @ u - u * hw, axis=0).max() / hw[0]
     assert abs(rel[0].item() - r) <= 1e-6 * r + 1e-15
     # nearly diagonal H: Newton refinement steps, few or no Jacobi sweeps
@@ -875,3 +882,32 @@ def test_small64_fp32_register_blocked(P, beta):
     B = host(b).reshape(P, n, n).transpose(0, 2, 1)
     want = (1.5 * (A @ B)).transpose(0, 2, 1).reshape(-1) + beta * host(dev(hc, torch.float32))
     assert naive.max_rel_err(host(c), want) <= TOL[torch.float32]
+
+
+@pytest.mark.parametrize("m,n,k,opa,opb", [(1024, 32, 512, "T", "N"), (512, 32, 1024, "N", "N"),
+                                           (64, 32, 512, "T", "N"), (200, 40, 333, "N", "T"),
+                                           (48, 700, 96, "T", "T"), (16384, 32, 512, "N", "N")])
+def test_skinny_fp64_products(m, n, k, opa, opb):
+    """fp64 products with a narrow side (the HOOI rank-p products) run on the
+    skinny DMMA kernel (in-kernel split-K, fixed reduction order): parity with
+    the oracle at 1e-12 and bitwise-reproducible."""
+    rng = np.random.default_rng(m * 7 + n + k)
+    lda = m if opa == "N" else k
+    ldb = k if opb == "N" else n
+    ha = rng.uniform(-1, 1, m * k)
+    hb = rng.uniform(-1, 1, k * n)
+    hc = rng.uniform(-1, 1, m * n)
+    a, b = dev(ha, torch.float64), dev(hb, torch.float64)
+    outs = []
+    for _ in range(2):
+        c = dev(hc, torch.float64)
+        kernels.gemm(opa, opb, m, n, k, 0.75, a, lda, b, ldb, 0.5, c, m)
+        outs.append(c)
+    assert _lib.last_kernel() == "skinny_dmma_f64", _lib.last_kernel()
+    assert torch.equal(outs[0], outs[1])
+    # column-major buffers: A is m x k (N, ld m) or stored k x m (T, ld k)
+    A = ha.reshape(k, m).T if opa == "N" else ha.reshape(m, k)
+    B = hb.reshape(n, k).T if opb == "N" else hb.reshape(k, n)
+    want = 0.75 * A @ B + 0.5 * hc.reshape(n, m).T
+    got = host(outs[0]).reshape(n, m).T
+    assert naive.max_rel_err(got, want) <= TOL[torch.float64]

@@ -33,7 +33,7 @@ int main() {
     long long z[2] = {0, 0};
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemcpyToSymbol(ritz::g_ritz_clock, z, sizeof(z));
-      ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES>>>(dq, dm, n, p, 32, 1e-7, du, nullptr, dw, df, drel);
+      ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES>>>(dq, dm, n, p, 32, 1e-7, du, nullptr, nullptr, dw, df, drel);
       cudaDeviceSynchronize();
     }
     long long c[2];

@@ -23,8 +23,8 @@ for n, p, warm in ((512, 32, True), (512, 48, True), (512, 32, False), (512, 48,
     w = torch.empty(rank, dtype=torch.float64, device="cuda")
     fl = torch.empty(1, dtype=torch.int32, device="cuda")
     rel = torch.empty(6, dtype=torch.float64, device="cuda")
-    call = lambda: lib.sbt_ritz_f64(P_(dq.data_ptr()), P_(dm.data_ptr()), n, p, rank, 1e-7,
-                                    P_(ut.data_ptr()), None, P_(w.data_ptr()), P_(fl.data_ptr()),
+    call = lambda: lib.sbt_ritz_f64(P_(dq.data_ptr()), None, n, p, rank, 1e-7,
+                                    P_(ut.data_ptr()), None, None, P_(w.data_ptr()), P_(fl.data_ptr()),
                                     P_(rel.data_ptr()), None)
     call(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

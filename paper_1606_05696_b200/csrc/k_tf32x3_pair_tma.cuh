@@ -86,9 +86,16 @@ struct Geo {
   // The lo ring bounds how far conversion runs ahead of the MMAs: a lo slot
   // cycles through MMA retire -> commit -> converter -> full barrier (both
   // CTAs) -> MMA issue, ~2.4K cycles measured (SBT_TRACE).  Wide tiles spend
-  // 1536 cycles of MMA per K-block, so 2 slots cover it; narrow tiles need
-  // more (e.g. 192 cycles per K-block at BNT = 32).
-  static constexpr int LO_SLOTS = (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? 3 : 5);
+  // 1536 cycles of MMA per K-block, so 2 slots cover it; narrow tiles are
+  // HBM-paced (~700 cycles per K-block at BNT = 32), where 3 lo slots keep the
+  // converters ahead and leave 7 raw slots for TMA depth (measured on the
+  // 512^3 rank-32 Tucker products: 2 / 3 / 4 / 5 lo slots = 5.2 / 5.7 / 5.3 /
+  // 5.0 TB/s).
+#ifndef SBT_LO_NARROW
+#define SBT_LO_NARROW 3
+#endif
+  static constexpr int LO_SLOTS =
+      (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? 3 : SBT_LO_NARROW);
   // epilogue staging for the TMA-store epilogue: 2 x (128 rows x 32 columns)
   static constexpr int EPI_BYTES = BB ? 0 : 2 * 128 * 32 * 4;
   // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles

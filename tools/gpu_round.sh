@@ -14,6 +14,8 @@ for dt in f32 f64; do
   timeout 300 python bench.py --config small --dtype $dt > gpurun_out/bench_small_$dt.json 2>&1
   timeout 300 python bench.py --config order4 --dtype $dt > gpurun_out/bench_order4_$dt.json 2>&1
 done
-timeout 400 python bench.py --config hooi --steps 4 > gpurun_out/bench_hooi_f32.json 2>&1
+timeout 400 python bench.py --config hooi > gpurun_out/bench_hooi_f32.json 2>&1
+timeout 400 python bench.py --config hooi --dtype f64 > gpurun_out/bench_hooi_f64.json 2>&1
+timeout 300 python bench.py --config conventional --no-e2e > gpurun_out/bench_conventional_f32.json 2>&1
 bash tools/profile_round.sh
 ls -la gpurun_out

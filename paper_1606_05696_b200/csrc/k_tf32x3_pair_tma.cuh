@@ -468,12 +468,13 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
           if (f.fm == 1) rb = x; else rb2 = x;
         }
         const uint32_t acc_col = b * ACC_W;
+        // TMEM loads run one chunk ahead: chunk cc + 32 is in flight while
+        // chunk cc is staged and stored
+        uint32_t v[32];
+        ptx::tmem_ld16(tmem + lane_addr + acc_col, *reinterpret_cast<uint32_t(*)[16]>(v));
+        ptx::tmem_ld16(tmem + lane_addr + acc_col + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
 #pragma unroll 1
         for (int cc = 0; cc < BNT; cc += 32, ++nchunk) {
-          uint32_t v[32];
-          ptx::tmem_ld16(tmem + lane_addr + acc_col + cc, *reinterpret_cast<uint32_t(*)[16]>(v));
-          ptx::tmem_ld16(tmem + lane_addr + acc_col + cc + 16,
-                         *reinterpret_cast<uint32_t(*)[16]>(v + 16));
           float o[32];
           if (SPLIT_ACC) {
             uint32_t w[32];
@@ -489,6 +490,12 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) o[j] = p.alpha * __uint_as_float(v[j]);
+          }
+          if (cc + 32 < BNT) {
+            ptx::tmem_ld16(tmem + lane_addr + acc_col + cc + 32,
+                           *reinterpret_cast<uint32_t(*)[16]>(v));
+            ptx::tmem_ld16(tmem + lane_addr + acc_col + cc + 48,
+                           *reinterpret_cast<uint32_t(*)[16]>(v + 16));
           }
           if (cc + 32 == BNT) {  // accumulator buffer drained: hand it back to the MMA
             ptx::tc_fence_before();

@@ -76,7 +76,7 @@ constexpr int kGroupWarps = 4;
 // double-buffered split accumulators).  BNT = 32 serves the rank-32 Tucker
 // products (M' = 262144, N = 32), which are HBM-bound: the MMA's shared-memory
 // reads per flop grow as N shrinks, but the tile still outruns HBM.
-template <int BK, bool BB = false, int BNT = 256>
+template <int BK, bool BB = false, int BNT = 256, int EPIB = 2>
 struct Geo {
   static constexpr int A_BYTES = 128 * BK * 4;               // A half (128 rows)
   static constexpr int B_BYTES = (BNT / 2) * BK * 4;         // B half (BNT/2 columns)
@@ -96,8 +96,11 @@ struct Geo {
 #endif
   static constexpr int LO_SLOTS =
       (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? 3 : SBT_LO_NARROW);
-  // epilogue staging for the TMA-store epilogue: 2 x (128 rows x 32 columns)
-  static constexpr int EPI_BYTES = BB ? 0 : 2 * 128 * 32 * 4;
+  // epilogue staging for the TMA-store epilogue: EPIB x (128 rows x 32
+  // columns).  Each buffer is one TMA store in flight: short-K tiles (K <= 128,
+  // e.g. the 4th-order contraction) are bound by the C writes, which need ~64 KB
+  // in flight per SM, so they take 4 buffers at the price of raw-ring depth
+  static constexpr int EPI_BYTES = BB ? 0 : EPIB * 128 * 32 * 4;
   // as many raw slots as fit in 227 KB: TMA latency under load is ~4.3K cycles
   // (measured), ~3 K-blocks of MMA time, and a raw slot stays held until the
   // MMAs that read it retire
@@ -117,6 +120,8 @@ struct Geo {
 __device__ long long g_trace[8][4096];
 #define TRACE(row, idx) do { if (blockIdx.x < 2 && (idx) < 4096) g_trace[(row) + 4 * rank][(idx)] = clock64(); } while (0)
 __device__ long long g_trace_epi[2][64][4];
+__device__ long long g_trace_mma[64][2];       // per tile: accumulator acquired, last commit
+__device__ long long g_trace_tepi[2][64][8];   // TMA-store epilogue: wait, acquired, released, end, phase sums
 #else
 #define TRACE(row, idx) do { } while (0)
 #endif
@@ -200,7 +205,7 @@ __device__ __forceinline__ void tma_operand(bool kmaj, const CUtensorMap* tm, ui
   }
 }
 
-template <int MAXP, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256>
+template <int MAXP, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256, int EPIB = 2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefetch) {
   const Problem* __restrict__ prs = ps.pr;
@@ -212,7 +217,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     if constexpr (MAXP == 1) { (void)t; (void)cur; return ps.pr[0]; }
     else return locate(prs, nprob, t, cur);
   };
-  using Gm = Geo<BK, BB, BNT>;
+  using Gm = Geo<BK, BB, BNT, EPIB>;
   constexpr int HNT = BNT / 2;  // B columns per CTA (MN-major B needs HNT >= 32: host-checked)
   constexpr int RAW_SLOTS = Gm::RAW_SLOTS, LO_SLOTS = Gm::LO_SLOTS;
   constexpr int OP_BYTES = Gm::OP_BYTES, SLOT_BYTES = Gm::SLOT_BYTES;
@@ -453,19 +458,32 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       const Tile tc = tile_of<BB, BNT>(t - P.tile_begin, P.tiles_m, P.tiles_n, P.nbatch);
     if (!BB && f.cmode) {
       // TMA-store epilogue: per 32-column chunk, TMEM -> registers (alpha) ->
-      // smem staging (double-buffered) -> one TMA store of a 128 x 32 box.
+      // per-warp smem staging (EPIB buffers) -> one TMA store of a 32 x 32 box
+      // per warp.
       // The TMA engine writes full lines and clips the M / N tails.
       {
         const uint32_t b = NBUF == 2 ? (tcount & 1u) : 0u;
         const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
+#ifdef SBT_TRACE
+        const long long tt0 = clock64();
+#endif
         ptx::mbar_wait(&acc_full[b], ph);
         ptx::tc_fence_after();
+#ifdef SBT_TRACE
+        const long long tt1 = clock64();
+        long long tt2 = 0, ph_ld = 0, ph_bw = 0, ph_st = 0;
+#endif
         // CTA row block -> (inner row, folded batch index)
         int64_t row0 = tc.m0 + rank * HM, rb = tc.pb, rb2 = tc.qb;
         if (f.fm) {
           const int64_t x = row0 / f.m_in;
           row0 -= x * f.m_in;
           if (f.fm == 1) rb = x; else rb2 = x;
+        }
+        int64_t ecol = tc.n0, ecy = 0;  // tile's first column, unfolded
+        if (f.fn) {
+          ecy = ecol / f.n_in;
+          ecol -= ecy * f.n_in;
         }
         const uint32_t acc_col = b * ACC_W;
         // TMEM loads run one chunk ahead: chunk cc + 32 is in flight while
@@ -476,6 +494,9 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
 #pragma unroll 1
         for (int cc = 0; cc < BNT; cc += 32, ++nchunk) {
           float o[32];
+#ifdef SBT_TRACE
+          const long long q0 = clock64();
+#endif
           if (SPLIT_ACC) {
             uint32_t w[32];
             ptx::tmem_ld16(tmem + lane_addr + acc_col + BNT + cc,
@@ -504,39 +525,69 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
               if (rank == 0) ptx::mbar_arrive(&acc_empty[b]);
               else ptx::mbar_arrive_remote(empty_leader[b]);
             }
+#ifdef SBT_TRACE
+            tt2 = clock64();
+#endif
           }
-          const uint32_t buf = nchunk & 1u;
-          const uint32_t stg = ptx::smem_addr(epi_stage + buf * (128 * 32 * 4));
-          if (leader) ptx::bulk_wait_group_read<1>();  // the store that used `buf` read it
-          ptx::named_bar_sync(1, 128);
-          if (f.cmode == 1) {  // [32 cols][128 rows]: a warp writes 128 B per column
+          // each warp stages and stores its own 32 rows (a 32 x 32 box): no
+          // barrier between the four epilogue warps
+          const uint32_t buf = nchunk % uint32_t(EPIB);
+          uint8_t* stg_p = epi_stage + (warp * EPIB + buf) * (32 * 32 * 4);
+          const uint32_t stg = ptx::smem_addr(stg_p);
+#ifdef SBT_TRACE
+          const long long q1 = clock64();
+#endif
+          if (lane == 0) ptx::bulk_wait_group_read<EPIB - 1>();  // the store that used `buf` read it
+          __syncwarp();
+#ifdef SBT_TRACE
+          const long long q2 = clock64();
+#endif
+          if (f.cmode == 1) {  // [32 cols][32 rows]: 128 B per column
 #pragma unroll
-            for (int j = 0; j < 32; ++j) ptx::sts_f32(stg + j * 512 + r * 4, o[j]);
-          } else {  // [128 rows][32 cols], 128 B swizzle (16 B chunk q at q ^ (row & 7))
+            for (int j = 0; j < 32; ++j) ptx::sts_f32(stg + j * 128 + lane * 4, o[j]);
+          } else {  // [32 rows][32 cols], 128 B swizzle (16 B chunk q at q ^ (row & 7))
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              ptx::sts_v4(stg + r * 128 + ((q ^ (r & 7)) << 4), __float_as_uint(o[4 * q]),
+              ptx::sts_v4(stg + lane * 128 + ((q ^ (lane & 7)) << 4), __float_as_uint(o[4 * q]),
                           __float_as_uint(o[4 * q + 1]), __float_as_uint(o[4 * q + 2]),
                           __float_as_uint(o[4 * q + 3]));
           }
           ptx::fence_proxy_async_smem();
-          ptx::named_bar_sync(1, 128);
-          if (leader) {
-            int64_t col0 = tc.n0 + cc, cb = rb, cb2 = rb2;
+          __syncwarp();
+#ifdef SBT_TRACE
+          const long long q3 = clock64();
+          ph_ld += q1 - q0;
+          ph_bw += q2 - q1;
+          ph_st += q3 - q2;
+#endif
+          if (lane == 0) {
+            // (un)fold the chunk's first column: one division per tile, then a
+            // carry per chunk (32 | n_in for N folds)
+            int64_t col0 = ecol + cc, cb = rb, cb2 = rb2;
             if (f.fn) {
-              const int64_t y = col0 / f.n_in;
-              col0 -= y * f.n_in;
+              int64_t y = ecy;
+              while (col0 >= f.n_in) col0 -= f.n_in, ++y;
               if (f.fn == 1) cb = y; else cb2 = y;
             }
+            const int wrow = int(row0) + 32 * warp;
             if (f.cmode == 1)
-              ptx::tma_store_4d(&P.tc, epi_stage + buf * (128 * 32 * 4), int(row0), int(col0),
-                                int(cb), int(cb2));
+              ptx::tma_store_4d(&P.tc, stg_p, wrow, int(col0), int(cb), int(cb2));
             else
-              ptx::tma_store_4d(&P.tc, epi_stage + buf * (128 * 32 * 4), int(col0), int(row0),
-                                int(cb), int(cb2));
+              ptx::tma_store_4d(&P.tc, stg_p, int(col0), wrow, int(cb), int(cb2));
             ptx::bulk_commit_group();
           }
         }
+#ifdef SBT_TRACE
+        if (blockIdx.x < 2 && tid == 0 && tcount < 64) {
+          g_trace_tepi[rank][tcount][0] = tt0;
+          g_trace_tepi[rank][tcount][1] = tt1;
+          g_trace_tepi[rank][tcount][2] = tt2;
+          g_trace_tepi[rank][tcount][3] = clock64();
+          g_trace_tepi[rank][tcount][4] = ph_ld;
+          g_trace_tepi[rank][tcount][5] = ph_bw;
+          g_trace_tepi[rank][tcount][6] = ph_st;
+        }
+#endif
       }
     } else {
     {
@@ -630,7 +681,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     }
     }  // direct-store epilogue
     }  // tiles
-    if (leader) ptx::bulk_wait_group<0>();
+    if (lane == 0) ptx::bulk_wait_group<0>();  // each warp's own stores
   } else if (warp == 13 && rank == 0) {
     // -------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (waits and descriptor math are
@@ -657,6 +708,9 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_empty[b], ph ^ 1u);
       ptx::tc_fence_after();
+#ifdef SBT_TRACE
+      if (blockIdx.x < 2 && tcount < 64) g_trace_mma[tcount][0] = clock64();
+#endif
       const uint32_t d_main = tmem + b * ACC_W;
       const uint32_t d_small = SPLIT_ACC ? d_main + BNT : d_main;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -692,6 +746,9 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       }
       if (ptx::elect_one_sync()) ptx::tc_commit2_mc(&acc_full[b], 0x3);
       __syncwarp();
+#ifdef SBT_TRACE
+      if (blockIdx.x < 2 && tcount < 64) g_trace_mma[tcount][1] = clock64();
+#endif
     }
   }
 

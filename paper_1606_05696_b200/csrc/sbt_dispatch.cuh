@@ -241,13 +241,14 @@ static bool fill_problem(const PairPlan& pl, tf32tma::Problem* pr) {
   // (128-row store boxes: not with an M fold of fewer rows per batch entry)
   if (!BB && tma_epi && p.beta == 0.f && aligned16(p.c) && vmult<float>(p.cps) &&
       vmult<float>(p.cps2) && !(f.fm && f.m_in % tf32tma::HM != 0)) {
+    // 32 x 32 boxes: each epilogue warp stores its own 32 rows
     if (p.crs == 1 && vmult<float>(p.ccs) &&
-        make_tmap_f32(&pr->tc, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 128, 32,
+        make_tmap_f32(&pr->tc, p.c, p.m, p.n, p.ccs, p.batch, p.cps, p.batch2, p.cps2, 32, 32,
                       CU_TENSOR_MAP_SWIZZLE_NONE))
       f.cmode = 1;
     else if (p.ccs == 1 && vmult<float>(p.crs) &&
              make_tmap_f32(&pr->tc, p.c, p.n, p.m, p.crs, p.batch, p.cps, p.batch2, p.cps2, 32,
-                           128, CU_TENSOR_MAP_SWIZZLE_128B))
+                           32, CU_TENSOR_MAP_SWIZZLE_128B))
       f.cmode = 2;
   }
   pr->p = p;
@@ -263,12 +264,12 @@ static bool fill_problem(const PairPlan& pl, tf32tma::Problem* pr) {
 }
 
 // Launch one problem set (tile_begin of each problem must be set, total summed).
-template <int MAXP, bool SPLIT, bool BB, int BNT, int KB = 32>
+template <int MAXP, bool SPLIT, bool BB, int BNT, int KB = 32, int EPIB = 2>
 static int launch_pair_set(const tf32tma::ProblemSet<MAXP>& ps, cudaStream_t stream,
                            const char* name) {
   static_assert(sizeof(tf32tma::ProblemSet<MAXP>) <= 32000, "kernel parameter space");
-  auto kern = tf32tma::tf32x3_pair_tma_kernel<MAXP, SPLIT, KB, BB, BNT>;
-  constexpr int smem = tf32tma::Geo<KB, BB, BNT>::SMEM_BYTES;
+  auto kern = tf32tma::tf32x3_pair_tma_kernel<MAXP, SPLIT, KB, BB, BNT, EPIB>;
+  constexpr int smem = tf32tma::Geo<KB, BB, BNT, EPIB>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -304,8 +305,15 @@ static int launch_pair_single_t(const PairPlan& pl, cudaStream_t stream) {
   ps.n = 1;
   ps.total = ps.pr[0].tiles_m * ps.pr[0].tiles_n * ps.pr[0].nbatch *
              ((ps.pr[0].f.fm == 2 || ps.pr[0].f.fn == 2) ? 1 : pl.p.batch2);
-  return launch_pair_set<1, SPLIT, BB, BNT>(
-      ps, stream, pair_name(BB, SPLIT, BNT, pl.f.fm || pl.f.fn, false));
+  const char* name = pair_name(BB, SPLIT, BNT, pl.f.fm || pl.f.fn, false);
+  // short K with the TMA-store epilogue: the C writes bound the tile, so more
+  // stores in flight (4 staging buffers) beat raw-ring depth
+  if constexpr (!SPLIT && !BB && BNT == 256) {
+    static const int epib4 = env_int("SBT_TC_EPIB4", 0);  // measured: no gain (kept for A/B)
+    if (epib4 && ps.pr[0].nkb <= 4 && ps.pr[0].f.cmode != 0)
+      return launch_pair_set<1, SPLIT, BB, BNT, 32, 4>(ps, stream, name);
+  }
+  return launch_pair_set<1, SPLIT, BB, BNT>(ps, stream, name);
 }
 
 // dispatch on the compile-time configuration of a plan

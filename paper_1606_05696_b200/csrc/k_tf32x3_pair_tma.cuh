@@ -94,8 +94,11 @@ struct Geo {
 #ifndef SBT_LO_NARROW
 #define SBT_LO_NARROW 3
 #endif
+#ifndef SBT_LO_128
+#define SBT_LO_128 3
+#endif
   static constexpr int LO_SLOTS =
-      (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? 3 : SBT_LO_NARROW);
+      (BK == 32 ? 1 : 2) * (BNT >= 256 ? 2 : BNT >= 128 ? SBT_LO_128 : SBT_LO_NARROW);
   // epilogue staging for the TMA-store epilogue: EPIB x (128 rows x 32
   // columns).  Each buffer is one TMA store in flight: short-K tiles (K <= 128,
   // e.g. the 4th-order contraction) are bound by the C writes, which need ~64 KB

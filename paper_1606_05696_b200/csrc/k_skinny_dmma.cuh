@@ -1,4 +1,4 @@
-// Skinny fp64 GEMMs (N <= 64 after orientation, no batch): the HOOI factor
+// Skinny fp64 GEMMs (N <= 64 after orientation): the HOOI factor
 // update's rank-p products (Y^T Q: 1024 x 32 x 512, Y W: 512 x 32 x 1024,
 // [Q Z]^T Z: 64 x 32 x 512).  The 128 x 128 DMMA tiles of k_dmma.cuh waste 3/4
 // of every tile on a 32-wide N and leave most SMs idle; here a CTA computes a
@@ -6,6 +6,8 @@
 // fragments), enough splits to fill the GPU, and the partial tiles are summed
 // in a fixed split order by the last CTA of each tile (an atomic ticket per
 // tile), so the result is deterministic and there is no second kernel.
+// Batched calls (fp64 Tucker mode products, N = rank) run one grid z-slice per
+// batch entry without splitting K.
 #pragma once
 #include "sbt_common.cuh"
 
@@ -52,8 +54,11 @@ __global__ void __launch_bounds__(NT) skinny_dmma_kernel(GemmParams<double> p, i
   const int64_t m0 = int64_t(tile % tiles_m) * BM, n0 = int64_t(tile / tiles_m) * BN;
   const int64_t kb = int64_t(split) * kper;
   const int64_t ke = kb + kper < p.k ? kb + kper : p.k;
-  const double* __restrict__ A = p.a;
-  const double* __restrict__ B = p.b;
+  // batched calls (no split): blockIdx.z = batch entry (batch2 outer)
+  const int64_t zb = blockIdx.z % p.batch, zq = blockIdx.z / p.batch;
+  const double* __restrict__ A = p.a + zb * p.aps + zq * p.aps2;
+  const double* __restrict__ B = p.b + zb * p.bps + zq * p.bps2;
+  double* __restrict__ Cz = p.c + zb * p.cps + zq * p.cps2;
 
   double acc[2][4][2];
 #pragma unroll
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(NT) skinny_dmma_kernel(GemmParams<double> p, i
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t col = n0 + j * 8 + 2 * fk + h;
-          if (col < p.n) store_out(p.c + row * p.crs + col * p.ccs, acc[i][j][h], p.alpha, p.beta);
+          if (col < p.n) store_out(Cz + row * p.crs + col * p.ccs, acc[i][j][h], p.alpha, p.beta);
         }
     }
     return;
@@ -193,8 +198,8 @@ __global__ void __launch_bounds__(NT) skinny_dmma_kernel(GemmParams<double> p, i
       const int e = 2 * (tid + (q0 + q) * NT);
       const int64_t row = m0 + e / BN, col = n0 + e % BN;
       if (row >= p.m) continue;
-      if (col < p.n) store_out(p.c + row * p.crs + col * p.ccs, sum[q].x, p.alpha, p.beta);
-      if (col + 1 < p.n) store_out(p.c + row * p.crs + (col + 1) * p.ccs, sum[q].y, p.alpha, p.beta);
+      if (col < p.n) store_out(Cz + row * p.crs + col * p.ccs, sum[q].x, p.alpha, p.beta);
+      if (col + 1 < p.n) store_out(Cz + row * p.crs + (col + 1) * p.ccs, sum[q].y, p.alpha, p.beta);
     }
   }
 }

@@ -773,9 +773,10 @@ static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
     attr = true;
   }
   const int64_t tiles_m = ceil_div(p.m, BM), tiles = tiles_m * ceil_div(p.n, BN);
-  if (tiles > 65535 * 16) return 0;
-  // splits: fill ~2 waves of CTAs, at least 2 K-chunks (of KC) per split
-  int64_t S = (2 * kNumSMs + tiles - 1) / tiles;
+  const int64_t nz = p.batch * p.batch2;
+  if (tiles > 65535 * 16 || nz > 65535) return 0;
+  // splits (unbatched only): fill ~2 waves of CTAs, at least 2 K-chunks per split
+  int64_t S = nz > 1 ? 1 : (2 * kNumSMs + tiles - 1) / tiles;
   const int64_t max_s = p.k / (2 * KC);
   if (S > max_s) S = max_s;
   if (S > 64) S = 64;
@@ -793,8 +794,8 @@ static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
     cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + wbytes);
     cudaMemsetAsync(cnt, 0, tiles * sizeof(unsigned), stream);
   }
-  kern<<<dim3(unsigned(tiles), unsigned(S)), NT, SMEM_BYTES, stream>>>(p, int(tiles_m), kper, ws,
-                                                                       cnt);
+  kern<<<dim3(unsigned(tiles), unsigned(S), unsigned(nz)), NT, SMEM_BYTES, stream>>>(
+      p, int(tiles_m), kper, ws, cnt);
   note_launch("skinny_dmma_f64");
   if (ws) cudaFreeAsync(ws, stream);
   return 1;
@@ -802,7 +803,10 @@ static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
 
 static int try_skinny_f64(const GemmParams<double>& p0, cudaStream_t stream) {
   static const int enabled = env_int("SBT_SKINNY", 1);
-  if (!enabled || p0.batch != 1 || p0.batch2 != 1 || p0.m == 1 || p0.n == 1) return 0;
+  if (!enabled || p0.m == 1 || p0.n == 1) return 0;
+  // batched: only when every entry fills a 64-row tile (the narrow side <= 64
+  // would waste most of a 128 x 128 DMMA tile)
+  if ((p0.batch > 1 || p0.batch2 > 1) && (p0.m < 64 && p0.n < 64)) return 0;
   // orientation with the narrow side as N
   const GemmParams<double> p = (p0.n <= skinny::BN * 2 || p0.m > skinny::BN * 2) ? p0
                                                                                   : transposed(p0);

@@ -911,3 +911,47 @@ def test_skinny_fp64_products(m, n, k, opa, opb):
     want = 0.75 * A @ B + 0.5 * hc.reshape(n, m).T
     got = host(outs[0]).reshape(n, m).T
     assert naive.max_rel_err(got, want) <= TOL[torch.float64]
+
+
+@pytest.mark.parametrize("m,n,k,P,bcast", [(512, 32, 512, 6, True), (96, 40, 200, 5, False),
+                                           (64, 64, 64, 7, False)])
+def test_skinny_fp64_batched(m, n, k, P, bcast):
+    """Batched fp64 products with a <= 64-wide side (fp64 Tucker mode products)
+    run on the skinny kernel, one grid slice per batch entry."""
+    rng = np.random.default_rng(m + n + k + P)
+    ha = rng.uniform(-1, 1, m * k * P)
+    hb = rng.uniform(-1, 1, k * n * (1 if bcast else P))
+    hc = rng.uniform(-1, 1, m * n * P)
+    a, b, c = dev(ha, torch.float64), dev(hb, torch.float64), dev(hc, torch.float64)
+    lob = 0 if bcast else k * n
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.25, a, m, m * k, b, k, lob, -0.5, c, m,
+                                 m * n, P)
+    assert _lib.last_kernel() == "skinny_dmma_f64", _lib.last_kernel()
+    want = host(dev(hc, torch.float64)).copy()
+    oapi.run_call("strided_batched_gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=1.25,
+                  lda=m, loa=m * k, ldb=k, lob=lob, beta=-0.5, ldc=m, loc=m * n, batch_count=P),
+                  host(a), host(b), want)
+    assert naive.max_rel_err(host(c), want) <= TOL[torch.float64]
+
+
+def test_hooi_graph_cache_reused_across_calls():
+    """A second hooi() on the same tensor replays the cached iteration graph
+    (no recapture) and reproduces the first call bitwise."""
+    from paper_1606_05696_b200 import tucker as tk
+    rng = np.random.default_rng(23)
+    dims, ranks = (192, 160, 128), (12, 8, 8)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    t = DenseTensor.from_array(full, dtype="float32")
+    tk.clear_graph_cache()
+    m1 = sbt.hooi(t, ranks, max_iters=6, tol=-1.0)
+    g1 = tk._IterationGraph._cache[1]
+    m2 = sbt.hooi(t, ranks, max_iters=6, tol=-1.0)
+    assert tk._IterationGraph._cache[1] is g1
+    assert m1.stats["graph"] and m2.stats["device_iterations"] >= 5
+    assert m1.fit_history == m2.fit_history
+    for u1, u2 in zip(m1.factors, m2.factors):
+        assert torch.equal(u1, u2)
+    tk.clear_graph_cache()
+    assert tk._IterationGraph._cache is None

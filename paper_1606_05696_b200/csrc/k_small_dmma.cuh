@@ -1,4 +1,4 @@
-// K3 (fp64, 16 < n <= 32): small-matrix batched GEMM on the DMMA pipe.
+// K3 (fp64, 16 < n <= 64): small-matrix batched GEMM on the DMMA pipe.
 //
 // The SIMT K3 kernel (k_small.cuh) reaches 0.93-0.95 of HBM bandwidth for fp64
 // n <= 16, but at n = 32 (AI = 2.7 flop/B) it is shared-memory bound: a 4x4
@@ -17,9 +17,13 @@
 // N = C row i), so each thread's accumulator pair is two consecutive rows of a
 // column of C: one 16-byte store.
 //
+// NMAX = 64 (32 < n <= 64, AI 5.3 flop/B: compute-bound in fp64): four warps
+// share one matrix, each owning a 32 x 32 quadrant of C^T; one matrix per
+// stage (70 KB), three stages.
+//
 // Requires A stored with rows contiguous (ars = 1, acs = m), B with k
 // contiguous (brs = 1, bcs = k), C dense (crs = 1, ccs = m); m, n multiples of
-// 8 and <= 32, k a multiple of 4 and <= 32 (checked by the dispatcher).
+// 8 and <= NMAX, k a multiple of 4 and <= NMAX (checked by the dispatcher).
 #pragma once
 #include <cuda.h>
 
@@ -31,13 +35,18 @@ namespace small_dmma {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int G = 4;        // matrices per group (one per warp)
 constexpr int STAGES = 3;
-constexpr int LD_MAX = 36;  // padded leading dimension for extents <= 32
 
 __host__ __device__ constexpr int ld_of(int rows) { return ((rows + 15) / 16) * 16 + 4; }
-__host__ __device__ constexpr int stage_doubles() { return G * 2 * LD_MAX * 32; }
-constexpr int SMEM_BYTES = STAGES * stage_doubles() * 8 + 64;
+template <int NMAX>
+struct Cfg {
+  static constexpr int Q = NMAX / 32;            // quadrants per side
+  static constexpr int WPM = Q * Q;              // warps per matrix
+  static constexpr int G = kWarps / WPM;         // matrices per group
+  static constexpr int LD_MAX = NMAX + 4;        // padded leading dimension
+  static constexpr int STAGE_DOUBLES = G * 2 * LD_MAX * NMAX;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + 64;
+};
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile(
@@ -55,9 +64,13 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
       : "memory");
 }
 
+template <int NMAX>
 __global__ void __launch_bounds__(kThreads, 1)
 small_dmma_kernel(GemmParams<double> p, const __grid_constant__ CUtensorMap tmA,
                   const __grid_constant__ CUtensorMap tmB, int64_t ngroups) {
+  using C_ = Cfg<NMAX>;
+  constexpr int G = C_::G;
+  auto stage_doubles = [] { return C_::STAGE_DOUBLES; };
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * stage_doubles() * 8);
@@ -96,10 +109,14 @@ small_dmma_kernel(GemmParams<double> p, const __grid_constant__ CUtensorMap tmA,
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int slot = int(it % STAGES);
     ptx::mbar_wait(&full[slot], (it / STAGES) & 1u);
-    const int64_t bidx = grp * G + warp;
+    const int mat = warp / C_::WPM, qw = warp % C_::WPM;
+    const int jq = qw / C_::Q, iq = qw % C_::Q;  // this warp's quadrant of C^T
+    const int64_t bidx = grp * G + mat;
     if (bidx < p.batch) {
-      const double* sa = sm + slot * stage_doubles() + warp * a_doubles;
-      const double* sb = sm + slot * stage_doubles() + G * a_doubles + warp * b_doubles;
+      const double* sa = sm + slot * stage_doubles() + mat * a_doubles + 32 * iq;
+      const double* sb = sm + slot * stage_doubles() + G * a_doubles + mat * b_doubles +
+                         32 * jq * ldb;
+      const int nt_q = nt - 4 * jq, mt_q = mt - 4 * iq;  // tiles in this quadrant
       double acc[4][4][2];  // [j tile][i tile][pair]
 #pragma unroll
       for (int jt = 0; jt < 4; ++jt)
@@ -111,23 +128,23 @@ small_dmma_kernel(GemmParams<double> p, const __grid_constant__ CUtensorMap tmA,
         // MMA B = A^T (4 l x 8 i): thread (l = r4, i = q8) -> A[i + l*lda]
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt)
-          fa[jt] = jt < nt ? sb[(l0 + r4) + (8 * jt + q8) * ldb] : 0.0;
+          fa[jt] = jt < nt_q ? sb[(l0 + r4) + (8 * jt + q8) * ldb] : 0.0;
 #pragma unroll
         for (int i2 = 0; i2 < 4; ++i2)
-          fb[i2] = i2 < mt ? sa[(8 * i2 + q8) + (l0 + r4) * lda] : 0.0;
+          fb[i2] = i2 < mt_q ? sa[(8 * i2 + q8) + (l0 + r4) * lda] : 0.0;
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt)
 #pragma unroll
           for (int i2 = 0; i2 < 4; ++i2)
-            if (jt < nt && i2 < mt) dmma(acc[jt][i2], fa[jt], fb[i2]);
+            if (jt < nt_q && i2 < mt_q) dmma(acc[jt][i2], fa[jt], fb[i2]);
       }
       // D[j][i] (j = 8 jt + q8, i = 8 i2 + 2 r4 + {0,1}) = C[i + j*ccs]
-      double* C = p.c + bidx * p.cps;
+      double* C = p.c + bidx * p.cps + 32 * iq + int64_t(32 * jq) * p.ccs;
 #pragma unroll
       for (int jt = 0; jt < 4; ++jt) {
 #pragma unroll
         for (int i2 = 0; i2 < 4; ++i2) {
-          if (jt >= nt || i2 >= mt) continue;
+          if (jt >= nt_q || i2 >= mt_q) continue;
           double* dst = C + (8 * i2 + 2 * r4) + int64_t(8 * jt + q8) * p.ccs;
           if (vec) {
             *reinterpret_cast<double2*>(dst) =

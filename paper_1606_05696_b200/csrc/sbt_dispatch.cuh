@@ -542,32 +542,41 @@ static int launch_small_s(const GemmParams<T>& p, bool am, bool bk, cudaStream_t
 }
 
 // fp64 16 < n <= 32 with column-major A, B and C: the DMMA variant of K3.
-static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
+template <int NMAX>
+static int launch_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
   using namespace small_dmma;
-  if (p.m % 8 || p.n % 8 || p.k % 4 || p.m > 32 || p.n > 32 || p.k > 32) return 0;
-  if (!(p.ars == 1 && p.acs == p.m && p.brs == 1 && p.bcs == p.k && p.crs == 1 && p.ccs == p.m))
-    return 0;
-  if (p.aps % 2 || p.bps % 2 || p.aps < p.m * p.k || p.bps < p.k * p.n) return 0;
-  if (!aligned16(p.a) || !aligned16(p.b) || p.batch > (int64_t(1) << 31)) return 0;
+  using C_ = Cfg<NMAX>;
+  auto kern = small_dmma_kernel<NMAX>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(small_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES) !=
+        cudaSuccess)
       return -3;
     attr_set = true;
   }
   CUtensorMap ta, tb;
   if (!make_tmap_f64_3d(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, ld_of(int(p.m)),
-                        uint32_t(p.k), G) ||
+                        uint32_t(p.k), C_::G) ||
       !make_tmap_f64_3d(&tb, p.b, p.k, p.n, p.bcs, p.batch, p.bps, ld_of(int(p.k)),
-                        uint32_t(p.n), G))
+                        uint32_t(p.n), C_::G))
     return 0;
-  const int64_t ngroups = ceil_div(p.batch, G);
+  const int64_t ngroups = ceil_div(p.batch, C_::G);
   const int64_t grid = ngroups < int64_t(kNumSMs) ? ngroups : int64_t(kNumSMs);
-  small_dmma_kernel<<<dim3(unsigned(grid)), dim3(kThreads), SMEM_BYTES, stream>>>(p, ta, tb,
-                                                                                 ngroups);
-  note_launch("small_batched_dmma_f64");
+  kern<<<dim3(unsigned(grid)), dim3(kThreads), C_::SMEM_BYTES, stream>>>(p, ta, tb, ngroups);
+  note_launch(NMAX == 32 ? "small_batched_dmma_f64" : "small_batched_dmma64_f64");
   return 1;
+}
+
+// fp64 16 < n <= 64 with column-major A, B and C: the DMMA variants of K3.
+static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
+  if (p.m % 8 || p.n % 8 || p.k % 4 || p.m > 64 || p.n > 64 || p.k > 64) return 0;
+  if (!(p.ars == 1 && p.acs == p.m && p.brs == 1 && p.bcs == p.k && p.crs == 1 && p.ccs == p.m))
+    return 0;
+  if (p.aps % 2 || p.bps % 2 || p.aps < p.m * p.k || p.bps < p.k * p.n) return 0;
+  if (!aligned16(p.a) || !aligned16(p.b) || p.batch > (int64_t(1) << 31)) return 0;
+  static const int use64 = env_int("SBT_SMALL_DMMA64", 1);
+  if (p.m > 32 || p.n > 32 || p.k > 32) return use64 ? launch_small_dmma<64>(p, stream) : 0;
+  return launch_small_dmma<32>(p, stream);
 }
 
 // fp32 64 x 64 x 64 batches with column-major A, B and C: 8 x 8 register blocks.
@@ -622,7 +631,7 @@ static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
   }
   if constexpr (sizeof(T) == 8) {
     static const int use_dmma = env_int("SBT_SMALL_DMMA", 1);
-    if (use_dmma && mx > 16 && mx <= 32) {
+    if (use_dmma && mx > 16 && mx <= 64) {
       const int rc = try_small_dmma(p, stream);
       if (rc != 0) return rc;
     }
@@ -807,6 +816,8 @@ static int try_skinny_f64(const GemmParams<double>& p0, cudaStream_t stream) {
   // batched: only when every entry fills a 64-row tile (the narrow side <= 64
   // would waste most of a 128 x 128 DMMA tile)
   if ((p0.batch > 1 || p0.batch2 > 1) && (p0.m < 64 && p0.n < 64)) return 0;
+  // many tiny matrices belong to the K3 small-matrix kernels
+  if (p0.batch >= 512 && p0.batch2 == 1 && p0.m <= 64 && p0.n <= 64 && p0.k <= 64) return 0;
   // orientation with the narrow side as N
   const GemmParams<double> p = (p0.n <= skinny::BN * 2 || p0.m > skinny::BN * 2) ? p0
                                                                                   : transposed(p0);

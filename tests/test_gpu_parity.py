@@ -955,3 +955,22 @@ def test_hooi_graph_cache_reused_across_calls():
         assert torch.equal(u1, u2)
     tk.clear_graph_cache()
     assert tk._IterationGraph._cache is None
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 64, 64), (48, 40, 64), (64, 24, 36), (40, 64, 20)])
+def test_small_dmma64_fp64(m, n, k):
+    """fp64 batches of matrices with an extent in (32, 64] run on the DMMA
+    small-matrix kernel (four warps per matrix) and match the oracle."""
+    P = 700
+    rng = np.random.default_rng(m * n + k)
+    ha, hb, hc = (rng.uniform(-1, 1, m * k * P), rng.uniform(-1, 1, k * n * P),
+                  rng.uniform(-1, 1, m * n * P))
+    a, b, c = dev(ha, torch.float64), dev(hb, torch.float64), dev(hc, torch.float64)
+    kernels.strided_batched_gemm("N", "N", m, n, k, 0.5, a, m, m * k, b, k, k * n, 2.0, c, m,
+                                 m * n, P)
+    assert _lib.last_kernel() == "small_batched_dmma64_f64", _lib.last_kernel()
+    want = host(dev(hc, torch.float64)).copy()
+    oapi.run_call("strided_batched_gemm", dict(opa="N", opb="N", m=m, n=n, k=k, alpha=0.5,
+                  lda=m, loa=m * k, ldb=k, lob=k * n, beta=2.0, ldc=m, loc=m * n, batch_count=P),
+                  host(a), host(b), want)
+    assert naive.max_rel_err(host(c), want) <= TOL[torch.float64]

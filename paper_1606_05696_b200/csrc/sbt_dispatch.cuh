@@ -199,8 +199,13 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
                          ((f.fm == 2 || f.fn == 2) ? 1 : q.batch2);
     const bool ok = variant == 4 ||
                     (f.mtot >= 256 && (f.ntot >= 96 || (f.ntot >= 16 && rows >= 8192 && qb == 1)));
+    // ties: prefer C unit-stride along N (vector staging stores in the
+    // TMA-store epilogue: 8 x 16 B per thread and chunk instead of 32 x 4 B)
+    static const int prefer_rowmajor_c = env_int("SBT_TC_PREFER_CN", 1);
+    const bool better_c = prefer_rowmajor_c && q.ccs == 1 && out->p.ccs != 1;
     if (ok && (!found || f.mtot > out->f.mtot ||
-               (f.mtot == out->f.mtot && f.ntot > out->f.ntot))) {
+               (f.mtot == out->f.mtot && (f.ntot > out->f.ntot ||
+                                          (f.ntot == out->f.ntot && better_c))))) {
       out->p = q; out->f = f; out->am = qa; out->bm = qb; found = true;
     }
   }

@@ -8,6 +8,9 @@ timeout 300 python bench.py > gpurun_out/bench_sweep_f32.json 2> gpurun_out/benc
 timeout 300 python bench.py --dtype f64 --no-e2e > gpurun_out/bench_sweep_f64.json 2> gpurun_out/bench_sweep_f64.err
 timeout 300 python bench.py --n 512 --no-e2e --no-cpu --steps 5 > gpurun_out/bench_sweep_f32_n512.json 2>&1
 timeout 300 python bench.py --n 128 --no-e2e --no-cpu > gpurun_out/bench_sweep_f32_n128.json 2>&1
+timeout 300 python bench.py --n 64 --no-e2e --no-cpu > gpurun_out/bench_sweep_f32_n64.json 2>&1
+timeout 300 python bench.py --n 64 --dtype f64 --no-e2e --no-cpu > gpurun_out/bench_sweep_f64_n64.json 2>&1
+timeout 300 python bench.py --n 512 --dtype f64 --no-e2e --no-cpu --steps 3 > gpurun_out/bench_sweep_f64_n512.json 2>&1
 timeout 300 python bench.py --n 1024 --no-e2e --no-cpu --steps 3 > gpurun_out/bench_sweep_f32_n1024.json 2>&1
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.json 2>&1
 for dt in f32 f64; do

@@ -215,6 +215,10 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
   if (out->bnt < 64 && out->bm != 1) return false;  // 16-column B halves must be K-major
   out->bb = false;
   out->split = pick_split(out->p);
+  // split accumulators (K > 512) fill TMEM at 256 columns: 128-wide tiles keep
+  // them double-buffered, so the epilogue overlaps the next tile's MMAs
+  static const int split_bnt = env_int("SBT_TC_SPLIT_BNT", 256);
+  if (out->split && out->bnt == 256 && split_bnt == 128) out->bnt = 128;
   return true;
 }
 

@@ -12,8 +12,9 @@ dispatcher semantics and executed as one launch of the sm_100a library.
 Weak scaling: every rank runs the full per-GPU sweep on its own operands (the
 batch/free-mode shard of a problem N times larger); there is no data-path
 collective.  value = FLOPs of all ranks / max-over-ranks device time.
-Inputs: 3 rotating operand sets per step, each larger than L2 at n >= 256, so
-consecutive cases never hit L2 for their operands.
+Inputs: 4 (or a multiple of the stream count) rotating operand sets per step,
+each larger than L2 at n >= 256, so consecutive cases never hit L2 for their
+operands; below n = 256 the working set fits L2 and the config line says so.
 """
 from __future__ import annotations
 
@@ -200,8 +201,17 @@ def run_gpu(args):
     # every case then needs its own C (36 x n^3 elements)
     # (n >= 512: one case is >= 0.5 ms, launch overheads are negligible and
     # separate launches on two streams fill each other's tails better)
-    group = (not args.no_group) and n <= 256
-    work = build_sets(cases, n, dtype, device, 4, seed=1234 + rank, distinct_c=group)
+    # (n <= 64: almost nothing is pair-groupable -- batched 64^3 problems with
+    # both operands batched -- and every case is ~1 us of work, so the cases go
+    # as separate launches spread over 8 streams, which overlap on the GPU:
+    # 2x the grouped single-stream rate, measured)
+    group = (not args.no_group) and 64 < n <= 256
+    if args.streams is None:
+        args.streams = 8 if n <= 64 else 2
+    # operand sets: a multiple of the stream count, so cases on different
+    # streams never share a buffer
+    nsets = 4 * ((args.streams + 3) // 4) if args.streams > 4 else 4
+    work = build_sets(cases, n, dtype, device, nsets, seed=1234 + rank, distinct_c=group)
     from paper_1606_05696_b200.planner import execute_plans
     exceptional = {cid for cid, *_ in work if cid in EXCEPTIONAL_CASES}
     stream = torch.cuda.current_stream(device)
@@ -425,7 +435,9 @@ def run_gpu(args):
             "config": {"workload": f"36-case single-index sweep (configs[1]) at n={n}",
                        "n": n, "cases": nc, "gflop_per_step_per_gpu": round(step_flops / 1e9, 2),
                        "parallelism": f"batch-sharded x{world} (no collective)",
-                       "l2": "4 rotating operand sets, each > L2 (126 MB) at n>=256",
+                       "l2": (f"{nsets} rotating operand sets, each > L2 (126 MB)" if n >= 256 else
+                              f"{nsets} rotating operand sets; at n={n} the working set fits "
+                              "L2, so inputs are L2-warm (no flush between steps)"),
                        "issue": ("one execute_plans call per step: the 36 independent "
                                  "contractions as grouped persistent launches (plain / "
                                  "exceptional)" if group else
@@ -763,7 +775,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--streams", type=int, default=None,
+                    help="CUDA streams for the step's launches (default 2; 8 for n <= 64)")
     ap.add_argument("--no-group", action="store_true",
                     help="issue the cases as separate calls instead of one grouped call")
     ap.add_argument("--sustained-probe", action="store_true",

@@ -201,13 +201,12 @@ def run_gpu(args):
     # every case then needs its own C (36 x n^3 elements)
     # (n >= 512: one case is >= 0.5 ms, launch overheads are negligible and
     # separate launches on two streams fill each other's tails better)
-    # (n <= 64: almost nothing is pair-groupable -- batched 64^3 problems with
-    # both operands batched -- and every case is ~1 us of work, so the cases go
-    # as separate launches spread over 8 streams, which overlap on the GPU:
-    # 2x the grouped single-stream rate, measured)
-    group = (not args.no_group) and 64 < n <= 256
+    # (n <= 64: almost nothing is pair-groupable and every case is ~1 us of
+    # work; execute_plans forks such calls over internal streams, so the step
+    # still overlaps its launches: 2x a single-stream issue, measured)
+    group = (not args.no_group) and n <= 256
     if args.streams is None:
-        args.streams = 8 if n <= 64 else 2
+        args.streams = 2
     # operand sets: a multiple of the stream count, so cases on different
     # streams never share a buffer
     nsets = 4 * ((args.streams + 3) // 4) if args.streams > 4 else 4

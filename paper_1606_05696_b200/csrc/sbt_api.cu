@@ -109,6 +109,25 @@ struct GroupRun {
   }
 };
 
+// internal streams for forking independent launches of a group (per host
+// thread; the events are re-recorded on every call)
+constexpr int kForkLanes = 8;
+struct ForkStreams {
+  cudaStream_t s[kForkLanes];
+  cudaEvent_t fork, join[kForkLanes];
+  ForkStreams() {
+    for (int l = 0; l < kForkLanes; ++l) {
+      cudaStreamCreateWithFlags(&s[l], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+  }
+};
+static ForkStreams& fork_streams() {
+  thread_local ForkStreams fs;
+  return fs;
+}
+
 template <typename T>
 static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream) {
   if (count < 0 || (count > 0 && !descs)) return fail(SBT_EINVAL, "group: bad arguments");
@@ -121,6 +140,10 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
     ps.push_back(p);
   }
   std::vector<char> launched(count, 0);
+  // fork point before any launch: forked calls (below) then overlap the
+  // grouped launches instead of queueing behind them
+  ForkStreams* fs = count >= 4 ? &fork_streams() : nullptr;
+  if (fs) cudaEventRecord(fs->fork, stream);
   if constexpr (sizeof(T) == 4) {
     if (kernel_override() == 0) {
       // bucket the pair-kernel problems by configuration (bb, split, bnt)
@@ -163,10 +186,28 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
       }
     }
   }
-  for (int i = 0; i < count; ++i) {  // everything not grouped: one call each
-    if (launched[i]) continue;
-    const int rc = run<T>(ps[i], stream);
+  // everything not grouped: one call each.  Many of them (small problems whose
+  // launches are mostly latency) fork onto internal streams and join back, so
+  // independent launches overlap on the GPU (capturable: event fork / join)
+  std::vector<int> rest;
+  for (int i = 0; i < count; ++i)
+    if (!launched[i]) rest.push_back(i);
+  if (!fs || rest.size() < 2) {
+    for (int i : rest) {
+      const int rc = run<T>(ps[i], stream);
+      if (rc != SBT_OK) return rc;
+    }
+    return check_cuda(cudaGetLastError(), "group launch");
+  }
+  const int lanes = int(rest.size()) < kForkLanes ? int(rest.size()) : kForkLanes;
+  for (int l = 0; l < lanes; ++l) cudaStreamWaitEvent(fs->s[l], fs->fork, 0);
+  for (size_t j = 0; j < rest.size(); ++j) {
+    const int rc = run<T>(ps[rest[j]], fs->s[j % lanes]);
     if (rc != SBT_OK) return rc;
+  }
+  for (int l = 0; l < lanes; ++l) {
+    cudaEventRecord(fs->join[l], fs->s[l]);
+    cudaStreamWaitEvent(stream, fs->join[l], 0);
   }
   return check_cuda(cudaGetLastError(), "group launch");
 }

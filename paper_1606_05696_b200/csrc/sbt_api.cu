@@ -115,17 +115,19 @@ constexpr int kForkLanes = 8;
 struct ForkStreams {
   cudaStream_t s[kForkLanes];
   cudaEvent_t fork, join[kForkLanes];
+  bool ok = true;
   ForkStreams() {
     for (int l = 0; l < kForkLanes; ++l) {
-      cudaStreamCreateWithFlags(&s[l], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
+      ok = ok && cudaStreamCreateWithFlags(&s[l], cudaStreamNonBlocking) == cudaSuccess;
+      ok = ok && cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming) == cudaSuccess;
     }
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    ok = ok && cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) cudaGetLastError();  // e.g. first use inside a stream capture: stay serial
   }
 };
-static ForkStreams& fork_streams() {
+static ForkStreams* fork_streams() {
   thread_local ForkStreams fs;
-  return fs;
+  return fs.ok ? &fs : nullptr;
 }
 
 template <typename T>
@@ -142,7 +144,7 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
   std::vector<char> launched(count, 0);
   // fork point before any launch: forked calls (below) then overlap the
   // grouped launches instead of queueing behind them
-  ForkStreams* fs = count >= 4 ? &fork_streams() : nullptr;
+  ForkStreams* fs = count >= 4 ? fork_streams() : nullptr;
   if (fs) cudaEventRecord(fs->fork, stream);
   if constexpr (sizeof(T) == 4) {
     if (kernel_override() == 0) {

@@ -2,26 +2,28 @@
 //
 // The reference takes the leading `rank` eigenvectors of each mode's Gram
 // matrix (tucker.py:63-76, Jacobi on the full n x n Gram, tucker.py:21-60).
-// HOOI here runs one warm-started subspace sweep per factor (tucker.py
-// top_eigh): Q = previous factor (n x p), Z = G Q, and M = [Q Z]^T Z give the
-// projected matrix H = Q^T G Q (p x p).  This kernel finishes the sweep
-// without a host round trip, so a whole HOOI iteration is launch-only:
-//   * cyclic Jacobi on H in shared memory (round-robin pairing: the p/2
-//     rotations of a step are independent, so a step is A <- J^T A J with J a
-//     product of disjoint rotations).  The index pairs of a step partition
-//     A and V into 2 x 2 blocks, each updated in place by one thread (A's
-//     upper triangle of blocks only, mirrored): 8 shared-memory loads and
-//     stores per 4 elements -- the fp64 step is shared-memory bound;
-//   * Ritz vectors from row tiles of Q and Z staged in shared memory (all
-//     loads of a tile in flight at once);
+// HOOI here runs warm-started subspace sweeps per factor (tucker.py
+// top_eigh): Q = previous factor (n x p), Z = G Q.  This kernel finishes a
+// sweep without a host round trip, so a whole HOOI iteration is launch-only.
+// One 8-CTA cluster:
+//   * H = Q^T Z (p x p): each CTA sums its row tiles of Q and Z, the partials
+//     are added in CTA order through distributed shared memory (or H comes
+//     from the caller's m = [Q Z]^T Z);
+//   * CTA 0 diagonalises H: Newton refinement for a warm start (A = V^T H V,
+//     V <- V (I + E) with E_ij = A_ij / (A_jj - A_ii), re-orthonormalised by
+//     one Newton-Schulz step; quadratic convergence in a few 32 x 32 products),
+//     then cyclic Jacobi for whatever is left (round-robin pairing: a step is
+//     A <- J^T A J with J a product of disjoint rotations; each 2 x 2 block of
+//     A and V is updated by one thread, one barrier per step);
 //   * eigenvalues sorted descending;
-//   * U = Q V, Y = Z V (= G U) for the leading `rank` Ritz vectors;
-//   * residuals ||Y_j - w_j U_j|| and the convergence flag
-//     max_j ||.|| <= tol * w_max (the same test as top_eigh);
+//   * all CTAs: U = Q V, Y = Z V (= G U) for the leading `rank` Ritz vectors
+//     from row tiles of Q and Z staged in shared memory; residuals
+//     ||Y_j - w_j U_j|| and the convergence flag max_j ||.|| <= tol * w_max
+//     (the same test as top_eigh);
 //   * sign rule of tucker.py:71-75 (largest |entry| of each column positive,
-//     first index on ties).
-// One CTA; p <= kMaxP.  The caller checks `flag` later (once per iteration)
-// and redoes the iteration on the host path if any factor did not converge.
+//     first index on ties), combined across the cluster; optional fp32 copy.
+// p <= kMaxP.  The caller checks `flag` later (once per iteration) and redoes
+// the iteration on the host path if any factor did not converge.
 #pragma once
 #include <cooperative_groups.h>
 

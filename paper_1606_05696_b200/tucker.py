@@ -18,7 +18,9 @@ Eigensolver: the reference's cyclic Jacobi (``tucker.py:21-60``) builds an
 n x n rotation per pivot and is infeasible at n = 512; ``jacobi_eigh`` here
 keeps its contract (values descending, matching eigenvector columns, symmetry
 check) but solves with the device's LAPACK-class ``torch.linalg.eigh``
-(cuSOLVER) in fp64.  This is off the contraction hot path.
+(cuSOLVER) in fp64; HOOI's warm factor updates instead finish their subspace
+sweeps on the device (``_factor_device``, k_ritz.cuh), one host round trip per
+iteration, replayed as a CUDA graph (``_IterationGraph``).
 """
 from __future__ import annotations
 

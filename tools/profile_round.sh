@@ -3,7 +3,7 @@
 # Reports stay in /tmp/prof on the box (too large to bring back); the counter
 # summaries land in gpurun_out/ (copied to profiles/ afterwards).
 mkdir -p gpurun_out /tmp/prof
-TAG=${TAG:-r01f}
+TAG=${TAG:-r01g}
 NCU="ncu --set full --clock-control none --import-source on"
 timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/pair_1.3_n256 -f python tools/case_single.py 1.3 256 f32 3 > /dev/null 2>&1
 timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o /tmp/prof/group_plain_n256 -f python tools/group_single.py plain 256 3 > /dev/null 2>&1

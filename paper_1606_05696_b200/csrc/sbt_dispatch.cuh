@@ -457,9 +457,15 @@ static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
   return 1;
 }
 
+// 16 warps per 128 x 128 tile (each 32 x 32) for short reductions, where a
+// tile's cp.async prologue and epilogue are a large share and more warps hide
+// them; 8 warps (64 x 32 each, more fragment reuse) for long ones.  Measured
+// (36-case fp64 sweeps, TF/s, 8 -> 16 warps): n=128 20.0 -> 23.9, n=256 27.7 ->
+// 27.7, n=512 29.7 -> 29.1, 4th order (K=128) 25.6 -> 26.1.
 template <bool AK, bool BK_, bool BB = false>
 static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
-  static const int nw = env_int("SBT_DMMA_WARPS", 8);
+  static const int nw_env = env_int("SBT_DMMA_WARPS", 0);  // 0 = by K
+  const int nw = nw_env ? nw_env : (p.k <= 256 ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
                   : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);
 }

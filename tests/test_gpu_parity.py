@@ -974,3 +974,27 @@ def test_small_dmma64_fp64(m, n, k):
                   lda=m, loa=m * k, ldb=k, lob=k * n, beta=2.0, ldc=m, loc=m * n, batch_count=P),
                   host(a), host(b), want)
     assert naive.max_rel_err(host(c), want) <= TOL[torch.float64]
+
+
+@pytest.mark.parametrize("m,n,k,P,ldc_pad", [(1000, 300, 96, 3, 0), (1000, 300, 96, 3, 8),
+                                             (4100, 256, 64, 1, 4), (520, 1030, 40, 2, 0)])
+def test_tma_store_epilogue_clips_tails(m, n, k, P, ldc_pad):
+    """beta = 0 pair-kernel calls use the per-warp TMA-store epilogue: row /
+    column tails that are not multiples of the 32 x 32 store box are clipped by
+    the tensor map, padded leading dimensions are respected (padding untouched)."""
+    rng = np.random.default_rng(m + n + ldc_pad)
+    ldc = m + ldc_pad
+    ha, hb = rng.uniform(-1, 1, m * k * P), rng.uniform(-1, 1, k * n * P)
+    a, b = dev(ha, torch.float32), dev(hb, torch.float32)
+    sentinel = 7.0
+    c = torch.full((ldc * n * P,), sentinel, dtype=torch.float32, device="cuda")
+    kernels.strided_batched_gemm("N", "N", m, n, k, 1.0, a, m, m * k, b, k, k * n, 0.0, c, ldc,
+                                 ldc * n, P)
+    assert _lib.last_kernel().startswith("tc_tf32x3_pair"), _lib.last_kernel()
+    A = ha.reshape(P, k, m).transpose(0, 2, 1)
+    B = hb.reshape(P, n, k).transpose(0, 2, 1)
+    want = np.einsum("pik,pkj->pij", A, B)
+    full = host(c).reshape(P, n, ldc).transpose(0, 2, 1)
+    assert naive.max_rel_err(full[:, :m, :], want) <= TOL[torch.float32]
+    if ldc_pad:
+        assert np.all(full[:, m:, :] == sentinel)

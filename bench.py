@@ -283,19 +283,12 @@ def run_gpu(args):
 
     def issue_step(main):
         if group:
-            # plain and exceptional cases as two grouped calls on two streams
-            # (their persistent launches overlap each other's tails)
-            subs = [[w for w in work if w[0] not in exceptional],
-                    [w for w in work if w[0] in exceptional]]
-            subs = [sb for sb in subs if sb]
-            lanes = [main] + side
-            for sd in side:
-                sd.wait_stream(main)
-            for i, sub in enumerate(subs):
-                with torch.cuda.stream(lanes[i % len(lanes)]):
-                    execute_plans([(plan, a, b, 1.0, 0.0, c) for cid, plan, a, b, c in sub])
-            for sd in side:
-                main.wait_stream(sd)
+            # the step's 36 independent contractions as ONE execute_plans call:
+            # the library runs each kernel configuration as one persistent launch
+            # (plain / exceptional) on its own internal stream and forks the
+            # remaining calls, joining back to this stream
+            with torch.cuda.stream(main):
+                execute_plans([(plan, a, b, 1.0, 0.0, c) for cid, plan, a, b, c in work])
             return
         for sd in side:
             sd.wait_stream(main)

@@ -131,7 +131,8 @@ static ForkStreams* fork_streams() {
 }
 
 template <typename T>
-static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream) {
+static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream_in) {
+  const cudaStream_t stream = stream_in;
   if (count < 0 || (count > 0 && !descs)) return fail(SBT_EINVAL, "group: bad arguments");
   std::vector<GemmParams<T>> ps;
   ps.reserve(count);
@@ -144,8 +145,17 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
   std::vector<char> launched(count, 0);
   // fork point before any launch: forked calls (below) then overlap the
   // grouped launches instead of queueing behind them
-  ForkStreams* fs = count >= 4 ? fork_streams() : nullptr;
+  ForkStreams* fs = count >= 2 ? fork_streams() : nullptr;
   if (fs) cudaEventRecord(fs->fork, stream);
+  bool forked = false;
+  int lane_next = 0;
+  auto lane = [&]() -> cudaStream_t {  // next internal stream (joined at the end)
+    if (!forked) {
+      for (int l = 0; l < kForkLanes; ++l) cudaStreamWaitEvent(fs->s[l], fs->fork, 0);
+      forked = true;
+    }
+    return fs->s[(lane_next++) % kForkLanes];
+  };
   if constexpr (sizeof(T) == 4) {
     if (kernel_override() == 0) {
       // bucket the pair-kernel problems by configuration (bb, split, bnt)
@@ -162,9 +172,14 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
                                  (pl.split ? 1 : 0));
         buckets[key].push_back(i);
       }
+      int nbuckets = 0;
+      for (int key = 0; key < 12; ++key) nbuckets += buckets[key].empty() ? 0 : 1;
       for (int key = 0; key < 12; ++key) {
         if (buckets[key].empty()) continue;
         const PairPlan& pl0 = plans[buckets[key][0]];
+        // independent configurations: their persistent launches overlap
+        // each other's tails on separate internal streams
+        const cudaStream_t stream = (fs && nbuckets >= 2) ? lane() : stream_in;
         int rc;
         if (pl0.bb && pl0.bnt == 128) {
           rc = pl0.split ? GroupRun<true, true, 128>::run(plans, buckets[key], stream, launched)
@@ -194,22 +209,16 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream)
   std::vector<int> rest;
   for (int i = 0; i < count; ++i)
     if (!launched[i]) rest.push_back(i);
-  if (!fs || rest.size() < 2) {
-    for (int i : rest) {
-      const int rc = run<T>(ps[i], stream);
-      if (rc != SBT_OK) return rc;
-    }
-    return check_cuda(cudaGetLastError(), "group launch");
-  }
-  const int lanes = int(rest.size()) < kForkLanes ? int(rest.size()) : kForkLanes;
-  for (int l = 0; l < lanes; ++l) cudaStreamWaitEvent(fs->s[l], fs->fork, 0);
-  for (size_t j = 0; j < rest.size(); ++j) {
-    const int rc = run<T>(ps[rest[j]], fs->s[j % lanes]);
+  const bool fork_rest = fs && (rest.size() >= 2 || (forked && !rest.empty()));
+  for (int i : rest) {
+    const int rc = run<T>(ps[i], fork_rest ? lane() : stream);
     if (rc != SBT_OK) return rc;
   }
-  for (int l = 0; l < lanes; ++l) {
-    cudaEventRecord(fs->join[l], fs->s[l]);
-    cudaStreamWaitEvent(stream, fs->join[l], 0);
+  if (forked) {
+    for (int l = 0; l < kForkLanes; ++l) {
+      cudaEventRecord(fs->join[l], fs->s[l]);
+      cudaStreamWaitEvent(stream, fs->join[l], 0);
+    }
   }
   return check_cuda(cudaGetLastError(), "group launch");
 }

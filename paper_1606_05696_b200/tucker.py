@@ -298,7 +298,7 @@ def _ritz_eligible(n: int, rank: int, warm) -> bool:
 
 
 def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
-                   sweeps: int = 1):
+                   sweeps: int = 1, out=None):
     """Warm-started subspace sweeps on the mode-r Gram, each finished on the
     device (``sbt_ritz_f64``): sweep 1 on the previous factor, further sweeps
     on the orthonormalised G U (one sweep reaches the fp32 tolerance after the
@@ -325,9 +325,13 @@ def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
         _gemm64(Op.Transpose, Op.Normal, cols, p, n, y, n, qz[:p], n, wbuf, cols)  # Y^T Q
         _gemm64(Op.Normal, Op.Normal, n, p, cols, y, n, wbuf, cols, qz[p:], n)     # Z = Y (Y^T Q)
         last = sweep == sweeps - 1
-        ut = torch.empty(rank, n, device=dev, dtype=torch.float64)
+        if last and out is not None:           # caller-owned (rank x n) buffers
+            ut, ut32 = out[0], (out[1] if not fp64 else None)
+        else:
+            ut = torch.empty(rank, n, device=dev, dtype=torch.float64)
+            ut32 = (torch.empty(rank, n, device=dev, dtype=torch.float32)
+                    if last and not fp64 else None)
         yt = None if last else torch.empty(rank, n, device=dev, dtype=torch.float64)
-        ut32 = torch.empty(rank, n, device=dev, dtype=torch.float32) if last and not fp64 else None
         w = torch.empty(rank, device=dev, dtype=torch.float64)
         rel = torch.empty(6, device=dev, dtype=torch.float64)
         flag = status[slot:] if last else torch.empty(1, device=dev, dtype=torch.int32)
@@ -461,16 +465,17 @@ def _hooi_sweep(t: DenseTensor, factors, fast: bool, factor_fn) -> DenseTensor:
 
 
 class _IterationGraph:
-    """One device-finished HOOI iteration captured as a CUDA graph (the
-    iteration is launch-only, so after the first capture a replay costs no
-    host work).  Static buffers: ``factors`` (read as the warm start, then
-    overwritten with the iteration's new factors), ``saved`` (the factors the
-    iteration started from, for the host-path redo) and ``out`` = [||G||,
-    convergence flags...]."""
+    """The device-finished HOOI iteration captured as a pair of CUDA graphs
+    (the iteration is launch-only, so a replay costs no host work).  The
+    factors live in two static buffer sets (fp64 rank x n rows, plus their
+    fp32 copies for fp32 tensors); graph 0 reads set 0 and its Ritz kernels
+    write set 1, graph 1 the reverse, so no factor is ever copied and the
+    iteration's starting factors stay intact for a host-path redo.  ``out`` of
+    each graph = [||G||, convergence flags...]."""
 
-    # the last captured iteration, reused by later hooi() calls on the same
-    # tensor buffer and configuration (capture and teardown cost milliseconds;
-    # holding the tensor's storage keeps the captured addresses valid)
+    # the last captured pair, reused by later hooi() calls on the same tensor
+    # buffer and configuration (capture and teardown cost milliseconds; holding
+    # the tensor's storage keeps the captured addresses valid)
     _cache = None
 
     @classmethod
@@ -480,8 +485,7 @@ class _IterationGraph:
         c = cls._cache
         if c is not None and c[0] == key:
             g = c[1]
-            for f, src in zip(g.factors, factors):
-                f.copy_(src)
+            g.load(factors)
             return g
         cls._cache = None
         g = cls.capture(t, factors, ranks, fast, sweeps)
@@ -489,52 +493,84 @@ class _IterationGraph:
             cls._cache = (key, g, t.data)
         return g
 
+    def _views(self, k):
+        """Factor views (dim x rank) of buffer set k, with their fp32 copies."""
+        vs = []
+        for u, u32 in zip(self.sets[k], self.sets32[k]):
+            v = u.t()
+            if u32 is not None:
+                v._sbt_f32 = u32
+            vs.append(v)
+        return vs
+
+    def load(self, factors):
+        """Make ``factors`` the starting point (set ``cur``)."""
+        for u, u32, f in zip(self.sets[self.cur], self.sets32[self.cur], factors):
+            u.copy_(f.t())
+            if u32 is not None:
+                u32.copy_(u)
+
+    @property
+    def factors(self):
+        return self._views(self.cur)
+
     @classmethod
     def capture(cls, t, factors, ranks, fast, sweeps):
         torch = _torch()
         self = cls()
         order = t.layout.order
-        self.factors = [f.contiguous().clone() for f in factors]
-        self.saved = [torch.empty_like(f) for f in self.factors]
-        self.status = torch.zeros(order, dtype=torch.int32, device=t.device)
-        self.graph = torch.cuda.CUDAGraph()
+        f32 = t.dtype == torch.float32
+        self.sets = [[torch.empty(f.shape[1], f.shape[0], device=t.device, dtype=torch.float64)
+                      for f in factors] for _ in range(2)]
+        self.sets32 = [[torch.empty_like(u, dtype=torch.float32) if f32 else None for u in st]
+                       for st in self.sets]
+        self.status = [torch.zeros(order, dtype=torch.int32, device=t.device) for _ in range(2)]
+        self.out = [None, None]
+        self.graphs = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+        self.cur = 0
         # capture_begin/end on a side stream directly: torch.cuda.graph() would
         # also gc.collect() and empty the caching allocator on every capture
         side = torch.cuda.Stream(device=t.device)
         side.wait_stream(torch.cuda.current_stream(t.device))
         try:
             with torch.cuda.stream(side):
-                self.graph.capture_begin()
-                try:
-                    self._record(t, ranks, fast, sweeps)
-                finally:
-                    self.graph.capture_end()
+                for k in range(2):
+                    self.graphs[k].capture_begin()
+                    try:
+                        self._record(k, t, ranks, fast, sweeps)
+                    finally:
+                        self.graphs[k].capture_end()
         except RuntimeError:      # something on the path is not capturable
             torch.cuda.synchronize()
             return None
         torch.cuda.current_stream(t.device).wait_stream(side)
+        self.load(factors)
         return self
 
-    def _record(self, t, ranks, fast, sweeps):
+    def _record(self, k, t, ranks, fast, sweeps):
         torch = _torch()
-        for sv, f in zip(self.saved, self.factors):
-            sv.copy_(f)
-        self.status.zero_()
-        work = list(self.factors)
-        core = _hooi_sweep(t, work, fast, lambda y, r, warm: _factor_device(
-            y, r, ranks[r], warm, self.status, r, sweeps))
+        st = self.status[k]
+        st.zero_()
+        nxt = 1 - k
+        outs = list(zip(self.sets[nxt], self.sets32[nxt]))
+        core = _hooi_sweep(t, self._views(k), fast, lambda y, r, warm: _factor_device(
+            y, r, ranks[r], warm, st, r, sweeps, out=outs[r]))
         norm_g = torch.linalg.vector_norm(core.data.to(torch.float64)).reshape(1)
-        self.out = torch.cat([norm_g, self.status.to(torch.float64)])
-        for f, u in zip(self.factors, work):
-            f.copy_(u)
+        self.out[k] = torch.cat([norm_g, st.to(torch.float64)])
 
     def replay(self):
-        self.graph.replay()
-        return self.out.cpu().numpy()
+        """One iteration from set ``cur`` into the other set; returns the
+        host copy of [||G||, flags] and advances ``cur`` (``factors`` are then
+        the new ones; ``previous`` the starting ones)."""
+        k = self.cur
+        self.graphs[k].replay()
+        vals = self.out[k].cpu().numpy()
+        self.cur = 1 - k
+        return vals
 
-    def restore(self):
-        for f, sv in zip(self.factors, self.saved):
-            f.copy_(sv)
+    @property
+    def previous(self):
+        return self._views(1 - self.cur)
 
 
 def clear_graph_cache() -> None:
@@ -578,10 +614,9 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
             sweeps = 2 if (it == 0 or t.dtype == torch.float64) else 1
             if graph is None and use_graph and it >= 1 and max_iters - it >= 3:
                 graph = _IterationGraph.get(t, factors, ranks, fast, sweeps)
-                if graph is not None:
-                    factors = graph.factors
             if graph is not None:
                 vals = graph.replay()                # one sync
+                factors = graph.factors
             else:
                 saved = list(factors)
                 status = torch.zeros(order, dtype=torch.int32, device=t.device)
@@ -596,11 +631,13 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
             else:                                    # an unconverged factor: host path
                 stats["host_redos"] += 1
                 if graph is not None:
-                    graph.restore()
-                    work = [f.clone() for f in factors]
+                    # the iteration's starting factors are intact in the
+                    # other buffer set: redo on the host path, make the result
+                    # the graph's current set
+                    work = [f.clone() for f in graph.previous]
                     core = _hooi_sweep(t, work, fast, host_factor)
-                    for f, u in zip(factors, work):
-                        f.copy_(u)
+                    graph.load(work)
+                    factors = graph.factors
                 else:
                     factors[:] = saved
                     core = _hooi_sweep(t, factors, fast, host_factor)

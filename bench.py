@@ -640,6 +640,20 @@ def run_config(args):
                            "hooi_paths": model.stats,
                            "contraction_gflop_per_iter": round(fl / 1e9, 2),
                            "fit_history": [round(f, 8) for f in model.fit_history]}}
+        # HBM roofline of the iteration's mode products (algorithmic bytes, each
+        # operand read and each product written once, mode-0 reuse): T twice,
+        # five n^2 r-sized tensors, four n r^2, the r^3 core
+        elems = 2 * n ** 3 + 5 * n * n * r + 4 * n * r * r + r ** 3
+        nbytes = it * elems
+        floor_ms = nbytes / (hbm * 1e9) * 1e3
+        line["roofline"] = {"bound": "hbm", "achieved": round(nbytes / per_iter / 1e9, 1),
+                            "peak": hbm, "unit": "GB/s",
+                            "frac": round(floor_ms / (per_iter * 1e3), 3), "traffic": None,
+                            "algorithmic_bytes_per_iter": nbytes,
+                            "floor_ms_per_iter": round(floor_ms, 4),
+                            "note": "bytes of the mode products only; the factor updates "
+                                    "(skinny fp64 products, Ritz kernels) add latency, "
+                                    "not bytes"}
     elif args.config == "conventional":
         # the paper's comparison (Fig. 1/4) on the device: every case
         # as planned (transpose-free, one launch) vs conventional

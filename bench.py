@@ -581,11 +581,26 @@ def run_config(args):
         launches = _lib.launch_count() - n0
         ms = _time_steps(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), args.steps, args.warmup)
         flops = 2.0 * n ** 5
+        kernel = _lib.last_kernel()
+        # roofline: the slower of the tensor pipe at its measured peak (3xTF32 =
+        # TF32 probe / 3; fp64 DMMA probe) and the operand + C bytes at HBM rate
+        if dtype == torch.float32:
+            tpeak, tsrc = _lib.probe_tf32_peak() / 3.0, "3xTF32 = measured tcgen05 TF32 / 3"
+        else:
+            tpeak, tsrc = _lib.probe_fp64_peak("dmma"), "measured DMMA"
+        nbytes = it * (2 * n ** 3 + n ** 4)
+        t_floor = max(flops / (tpeak * 1e12), nbytes / (hbm * 1e9)) * 1e3
         line = {"metric": "4th-order contraction GFLOP/s", "value": round(flops / (ms * 1e-3) / 1e9, 1),
                 "unit": "GFLOP/s", "ms_per_step": round(ms, 4),
+                "roofline": {"bound": "tensor" if flops / tpeak / 1e12 > nbytes / hbm / 1e9 else "hbm",
+                             "achieved": round(flops / (ms * 1e-3) / 1e12, 2), "peak": round(tpeak, 2),
+                             "unit": "TFLOP/s", "frac": round(t_floor / ms, 3), "traffic": None,
+                             "peak_source": tsrc, "hbm_peak_gbs": hbm,
+                             "algorithmic_bytes": nbytes,
+                             "note": "frac = max(flop / tensor peak, bytes / HBM) / measured time"},
                 "config": {"workload": f"configs[4] C[mnpq]=A[mkp]B[nkq] n={n}",
                            "strategy": plan.strategy, "launches_per_contraction": launches,
-                           "kernel": _lib.last_kernel()}}
+                           "kernel": kernel}}
     elif args.config == "hooi":
         import paper_1606_05696_b200 as sbt
         n, r = (args.n if args.n != 256 else 512), 32

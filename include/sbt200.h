@@ -13,8 +13,13 @@
  *
  * Units: element (not byte) offsets and strides, int64, all >= 0 (a zero batch
  * stride broadcasts that operand, reference test_kernels.py:84-96).
- * Ownership: A and B are read, C is updated in place; the library allocates
- * nothing on the device-pointer entry points.
+ * Ownership: A and B are read, C is updated in place.  Device memory on the
+ * device-pointer entry points: none for the contraction kernels themselves;
+ * the split-K paths (few output tiles with a long reduction, e.g. Gram
+ * matrices) draw a stream-ordered workspace from the device's default memory
+ * pool (cudaMallocAsync / cudaFreeAsync, capturable in a CUDA graph; the pool
+ * keeps released memory, so repeated calls of a shape do not allocate from the
+ * driver).  A failed workspace allocation returns SBT_ECUDA with a message.
  * Errors: 0 on success, a negative SBT_E* code otherwise; sbt_last_error()
  * returns a message for the calling thread.  The reference cores do no
  * validation (validation lives in kernels.py); these entry points validate

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,7 @@
 #include "sbt_common.cuh"
 #include "k_generic.cuh"
 #include "sbt_dispatch.cuh"
+#include "sbt_host.cuh"
 #include "k_probe.cuh"
 #include "k_permute.cuh"
 #include "k_ritz.cuh"
@@ -42,6 +44,24 @@ void note_launch(const char* name) {
 }
 
 int kernel_override() { return g_override.load(std::memory_order_relaxed); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SBT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int set_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return SBT_OK;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(max dynamic smem)");
+  done.insert({fn, dev});
+  return SBT_OK;
+}
 
 static int check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -68,8 +88,14 @@ static int run(GemmParams<T> p, cudaStream_t stream) {
   int rc = validate(p);
   if (rc != SBT_OK) return rc;
   if (p.batch == 0 || p.batch2 == 0) return SBT_OK;  // reference: batch 0 is a no-op
+  t_err.clear();
   rc = launch_gemm<T>(p, stream);
-  if (rc != SBT_OK) return rc;
+  if (rc != SBT_OK) {
+    if (t_err.empty())
+      return fail(rc, rc == SBT_EUNSUPPORTED ? "no kernel for this request (grid too large)"
+                                             : "kernel launch failed");
+    return rc;
+  }
   return check_cuda(cudaGetLastError(), "kernel launch");
 }
 
@@ -125,9 +151,18 @@ struct ForkStreams {
     if (!ok) cudaGetLastError();  // e.g. first use inside a stream capture: stay serial
   }
 };
+// one lane set per (host thread, device): streams belong to the device that
+// was current when they were created
+constexpr int kMaxDevices = 64;
 static ForkStreams* fork_streams() {
-  thread_local ForkStreams fs;
-  return fs.ok ? &fs : nullptr;
+  thread_local ForkStreams* per_dev[kMaxDevices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (!per_dev[dev]) per_dev[dev] = new ForkStreams();  // lives as long as the thread
+  return per_dev[dev]->ok ? per_dev[dev] : nullptr;
 }
 
 template <typename T>
@@ -146,13 +181,31 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream_
   // fork point before any launch: forked calls (below) then overlap the
   // grouped launches instead of queueing behind them
   ForkStreams* fs = count >= 2 ? fork_streams() : nullptr;
-  if (fs) cudaEventRecord(fs->fork, stream);
+  if (fs && cudaEventRecord(fs->fork, stream) != cudaSuccess) {
+    cudaGetLastError();
+    fs = nullptr;  // serial issue
+  }
   bool forked = false;
+  // join the internal lanes back into the caller's stream on EVERY exit path
+  // (an unjoined lane would invalidate an enclosing stream capture)
+  auto finish = [&](int rc) -> int {
+    if (forked) {
+      for (int l = 0; l < kForkLanes; ++l) {
+        const cudaError_t e1 = cudaEventRecord(fs->join[l], fs->s[l]);
+        const cudaError_t e2 = cudaStreamWaitEvent(stream, fs->join[l], 0);
+        if (rc == SBT_OK && e1 != cudaSuccess) rc = cuda_fail(e1, "group join (event record)");
+        if (rc == SBT_OK && e2 != cudaSuccess) rc = cuda_fail(e2, "group join (stream wait)");
+      }
+      forked = false;
+    }
+    if (rc != SBT_OK) return rc;
+    return check_cuda(cudaGetLastError(), "group launch");
+  };
   int lane_next = 0;
   auto lane = [&]() -> cudaStream_t {  // next internal stream (joined at the end)
     if (!forked) {
       for (int l = 0; l < kForkLanes; ++l) cudaStreamWaitEvent(fs->s[l], fs->fork, 0);
-      forked = true;
+      forked = true;  // (a failed wait surfaces in the final cudaGetLastError check)
     }
     return fs->s[(lane_next++) % kForkLanes];
   };
@@ -199,7 +252,7 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream_
                                     : GroupRun<false, false, 256>::run(plans, buckets[key], stream, launched); break;
           }
         }
-        if (rc < 0) return rc;
+        if (rc < 0) return finish(rc);
       }
     }
   }
@@ -212,26 +265,12 @@ static int run_group(int count, const sbt_gemm_desc* descs, cudaStream_t stream_
   const bool fork_rest = fs && (rest.size() >= 2 || (forked && !rest.empty()));
   for (int i : rest) {
     const int rc = run<T>(ps[i], fork_rest ? lane() : stream);
-    if (rc != SBT_OK) return rc;
+    if (rc != SBT_OK) return finish(rc);
   }
-  if (forked) {
-    for (int l = 0; l < kForkLanes; ++l) {
-      cudaEventRecord(fs->join[l], fs->s[l]);
-      cudaStreamWaitEvent(stream, fs->join[l], 0);
-    }
-  }
-  return check_cuda(cudaGetLastError(), "group launch");
+  return finish(SBT_OK);
 }
 
-// ---- host-buffer path -------------------------------------------------------
-struct DeviceArena {
-  std::mutex mu;
-  void* ptr = nullptr;
-  size_t bytes = 0;
-  int device = -1;
-};
-static DeviceArena g_arena;
-
+// ---- host-buffer path (re-entrant: see sbt_host.cuh) -------------------------
 static int64_t span_of(int64_t m, int64_t k, int64_t rs, int64_t cs, int64_t ps, int64_t batch) {
   return 1 + (m - 1) * rs + (k - 1) * cs + (batch > 0 ? (batch - 1) * ps : 0);
 }
@@ -252,39 +291,31 @@ static int run_host(int64_t m, int64_t n, int64_t k, T alpha, const T* a, int64_
   const bool c_dense = (nc == m * n * batch);
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t ba = align(na * sizeof(T)), bb = align(nb * sizeof(T)), bc = align(nc * sizeof(T));
-  std::lock_guard<std::mutex> lock(g_arena.mu);
-  int dev = 0;
-  if ((rc = check_cuda(cudaGetDevice(&dev), "cudaGetDevice")) != SBT_OK) return rc;
-  if (g_arena.device != dev || g_arena.bytes < ba + bb + bc) {
-    if (g_arena.ptr) cudaFree(g_arena.ptr);
-    g_arena.ptr = nullptr;
-    g_arena.bytes = 0;
-    if ((rc = check_cuda(cudaMalloc(&g_arena.ptr, ba + bb + bc), "cudaMalloc")) != SBT_OK)
-      return rc;
-    g_arena.bytes = ba + bb + bc;
-    g_arena.device = dev;
-  }
-  char* base = static_cast<char*>(g_arena.ptr);
+  cudaError_t e = cudaSuccess;
+  host::HostCtx* cx = host::ctx_for_current_device(&e);
+  if (!cx) return cuda_fail(e, "host seam: per-thread stream / staging buffers");
+  if ((e = cx->reserve(ba + bb + bc)) != cudaSuccess) return cuda_fail(e, "host seam: device arena");
+  char* base = static_cast<char*>(cx->arena);
   T* da = reinterpret_cast<T*>(base);
   T* db = reinterpret_cast<T*>(base + ba);
   T* dc = reinterpret_cast<T*>(base + ba + bb);
-  cudaStream_t s = 0;
-  if ((rc = check_cuda(cudaMemcpyAsync(da, a + oa, na * sizeof(T), cudaMemcpyHostToDevice, s),
-                       "H2D A")) != SBT_OK) return rc;
-  if ((rc = check_cuda(cudaMemcpyAsync(db, b + ob, nb * sizeof(T), cudaMemcpyHostToDevice, s),
-                       "H2D B")) != SBT_OK) return rc;
+  if ((e = host::upload(cx, da, a + oa, na * sizeof(T))) != cudaSuccess) return cuda_fail(e, "H2D A");
+  if ((e = host::upload(cx, db, b + ob, nb * sizeof(T))) != cudaSuccess) return cuda_fail(e, "H2D B");
   // C's span is copied in unless beta == 0 and the batch regions tile it exactly
   // (otherwise the gaps between regions must survive the copy back).
   if (beta != T(0) || !c_dense) {
-    if ((rc = check_cuda(cudaMemcpyAsync(dc, c + oc, nc * sizeof(T), cudaMemcpyHostToDevice, s),
-                         "H2D C")) != SBT_OK) return rc;
+    if ((e = host::upload(cx, dc, c + oc, nc * sizeof(T))) != cudaSuccess)
+      return cuda_fail(e, "H2D C");
   }
   GemmParams<T> p = make<T>(m, n, k, alpha, da, 0, ars, acs, apt, 0, db, 0, brs, bcs, bpt, 0,
                             beta, dc, 0, crs, ccs, cpt, 0, batch, 1);
-  if ((rc = run(p, s)) != SBT_OK) return rc;
-  if ((rc = check_cuda(cudaMemcpyAsync(c + oc, dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s),
-                       "D2H C")) != SBT_OK) return rc;
-  return check_cuda(cudaStreamSynchronize(s), "stream sync");
+  if ((rc = run(p, cx->stream)) != SBT_OK) {
+    cudaStreamSynchronize(cx->stream);  // leave the context idle for the next call
+    return rc;
+  }
+  if ((e = host::download(cx, c + oc, dc, nc * sizeof(T))) != cudaSuccess)
+    return cuda_fail(e, "D2H C");
+  return SBT_OK;
 }
 
 }  // namespace sbt
@@ -509,14 +540,9 @@ int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, 
   if (!qz || !ut || !w || !flag || !rel || n < 1 || p < 1 || p > ritz::kMaxP ||
       rank < 1 || rank > p || p > n)
     return fail(SBT_EINVAL, "sbt_ritz_f64: bad arguments");
-  static bool attr = false;
-  if (!attr) {
-    const int rc = check_cuda(cudaFuncSetAttribute(ritz::ritz_kernel,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   ritz::SMEM_BYTES),
-                              "cudaFuncSetAttribute");
+  {
+    const int rc = set_smem_attr(reinterpret_cast<const void*>(ritz::ritz_kernel), ritz::SMEM_BYTES);
     if (rc != SBT_OK) return rc;
-    attr = true;
   }
   ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
       qz, m, n, p, rank, tol, ut, yt, ut32, w, flag, rel);

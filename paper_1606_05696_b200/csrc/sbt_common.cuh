@@ -27,6 +27,11 @@ struct GemmParams {
 
 // Host-side bookkeeping shared by every launcher (defined in sbt_api.cu).
 void note_launch(const char* kernel_name);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the CURRENT device
+// (cached per (kernel, device)); 0 or SBT_ECUDA with sbt_last_error set.
+int set_smem_attr(const void* fn, int bytes);
+// record a CUDA failure of a launcher for sbt_last_error(); returns SBT_ECUDA
+int cuda_fail(cudaError_t e, const char* what);
 int kernel_override();  // 0 auto, 1 generic, 2 tensor-core tiled, 3 small-matrix
 constexpr int kNumSMs = 148;
 

@@ -96,13 +96,7 @@ template <int BN, bool AK, bool BK_>
 static int launch_tf32x3_cfg(const GemmParams<float>& p, cudaStream_t stream) {
   using C_ = tf32x3::Cfg<BN>;
   auto kern = tf32x3::tf32x3_gemm_kernel<BN, AK, BK_>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C_::SMEM_BYTES) != cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), C_::SMEM_BYTES) != 0) return -3;
   const int64_t tiles_m = ceil_div(p.m, tf32x3::BM), tiles_n = ceil_div(p.n, BN);
   const int64_t total = tiles_m * tiles_n * p.batch * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
@@ -279,13 +273,7 @@ static int launch_pair_set(const tf32tma::ProblemSet<MAXP>& ps, cudaStream_t str
   static_assert(sizeof(tf32tma::ProblemSet<MAXP>) <= 32000, "kernel parameter space");
   auto kern = tf32tma::tf32x3_pair_tma_kernel<MAXP, SPLIT, KB, BB, BNT, EPIB>;
   constexpr int smem = tf32tma::Geo<KB, BB, BNT, EPIB>::SMEM_BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), smem) != 0) return -3;
   const int64_t pairs = ps.total < kNumSMs / 2 ? ps.total : kNumSMs / 2;
   // low byte: L2 prefetch distance (measured: no gain, 0); bits 8/9: diagnostics
   // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
@@ -442,13 +430,7 @@ static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm
 template <bool AK, bool BK_, bool BB, int NW>
 static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
   auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dmma::SMEM_BYTES) != cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), dmma::SMEM_BYTES) != 0) return -3;
   const int64_t tiles_m = ceil_div(p.m, BB ? 32 : dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
   const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
@@ -533,13 +515,7 @@ template <typename T, int S, bool AM, bool BK_>
 static int launch_small_cfg(const GemmParams<T>& p, cudaStream_t stream) {
   auto kern = small::small_batched_kernel<T, S, AM, BK_>;
   constexpr int smem = small::smem_bytes<T, S>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), smem) != 0) return -3;
   const int64_t ngroups = ceil_div(p.batch, small::Shape<S>::G);
   const int per_sm = smem <= 110 * 1024 ? 2 : 1;
   const int64_t grid = ngroups < int64_t(kNumSMs) * per_sm ? ngroups : int64_t(kNumSMs) * per_sm;
@@ -562,13 +538,7 @@ static int launch_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
   using namespace small_dmma;
   using C_ = Cfg<NMAX>;
   auto kern = small_dmma_kernel<NMAX>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES) !=
-        cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), C_::SMEM_BYTES) != 0) return -3;
   CUtensorMap ta, tb;
   if (!make_tmap_f64_3d(&ta, p.a, p.m, p.k, p.acs, p.batch, p.aps, ld_of(int(p.m)),
                         uint32_t(p.k), C_::G) ||
@@ -603,13 +573,7 @@ static int try_small64(const GemmParams<float>& p, cudaStream_t stream) {
   if (p.aps % 4 || p.bps % 4 || p.aps < 4096 || p.bps < 4096 || !aligned16(p.a) ||
       !aligned16(p.b) || p.batch > (int64_t(1) << 31))
     return 0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(small64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES) != cudaSuccess)
-      return -3;
-    attr_set = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(small64_kernel), SMEM_BYTES) != 0) return -3;
   CUtensorMap ta, tb;
   if (!make_tmap_f32(&ta, p.a, 64, 64, 64, p.batch, p.aps, 1, 0, 64, 64,
                      CU_TENSOR_MAP_SWIZZLE_NONE, G) ||
@@ -711,9 +675,11 @@ static int try_split_k(const GemmParams<T>& p, cudaStream_t stream) {
     return true;
   }();
   (void)pool_kept;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&w), size_t(S) * p.m * p.n * sizeof(T), stream) !=
-      cudaSuccess)
-    return -3;
+  {
+    const cudaError_t e =
+        cudaMallocAsync(reinterpret_cast<void**>(&w), size_t(S) * p.m * p.n * sizeof(T), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "split-K workspace (cudaMallocAsync)");
+  }
   GemmParams<T> q = p;
   q.alpha = T(1); q.beta = T(0);
   q.c = w; q.crs = 1; q.ccs = p.m; q.cps = p.m * p.n;
@@ -789,13 +755,7 @@ template <bool AK, bool BK_>
 static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   using namespace skinny;
   auto kern = skinny_dmma_kernel<AK, BK_>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
-        cudaSuccess)
-      return -3;
-    attr = true;
-  }
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), SMEM_BYTES) != 0) return -3;
   const int64_t tiles_m = ceil_div(p.m, BM), tiles = tiles_m * ceil_div(p.n, BN);
   const int64_t nz = p.batch * p.batch2;
   if (tiles > 65535 * 16 || nz > 65535) return 0;
@@ -812,9 +772,9 @@ static int launch_skinny_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   if (S > 1) {
     keep_pool_memory();
     const size_t wbytes = size_t(tiles) * S * TILE * sizeof(double);
-    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + tiles * sizeof(unsigned),
-                        stream) != cudaSuccess)
-      return -3;
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws),
+                                          wbytes + tiles * sizeof(unsigned), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "skinny split-K workspace (cudaMallocAsync)");
     cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + wbytes);
     cudaMemsetAsync(cnt, 0, tiles * sizeof(unsigned), stream);
   }

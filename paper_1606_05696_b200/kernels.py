@@ -129,12 +129,12 @@ def _buffer_info(buf, name):
     return buf.dtype, buf.numel()
 
 
-def core_call(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta, c, oc,
-              crs, ccs, cpt, batch=1, apt2=0, bpt2=0, cpt2=0, batch2=1, extended=False):
-    """Launch C = alpha*A.B + beta*C over strided views (the reference core
-    signature, _loops_numba.py:12-35, plus an optional second batch mode)."""
-    if batch == 0 or batch2 == 0:
-        return
+def validate_call(m, n, k, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, c, oc, crs, ccs, cpt,
+                  batch=1, apt2=0, bpt2=0, cpt2=0, batch2=1):
+    """Buffer checks of one strided core call (every path into the library runs
+    them: core_call and the grouped planner.execute_plans): flat contiguous
+    buffers of one dtype on one side (host / device), non-negative strides, and
+    every addressed element inside its buffer.  Returns (dtype, is_host)."""
     da, na = _buffer_info(a, "A")
     db, nb = _buffer_info(b, "B")
     dc, nc = _buffer_info(c, "C")
@@ -152,6 +152,17 @@ def core_call(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta, 
             ("C", _span(oc, [(m, crs), (n, ccs), (batch, cpt), (batch2, cpt2)]), nc)):
         if top >= size:
             raise ValueError(f"{name}: call addresses element {top} of a buffer of {size}")
+    return da, host
+
+
+def core_call(m, n, k, alpha, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, beta, c, oc,
+              crs, ccs, cpt, batch=1, apt2=0, bpt2=0, cpt2=0, batch2=1, extended=False):
+    """Launch C = alpha*A.B + beta*C over strided views (the reference core
+    signature, _loops_numba.py:12-35, plus an optional second batch mode)."""
+    if batch == 0 or batch2 == 0:
+        return
+    da, host = validate_call(m, n, k, a, oa, ars, acs, apt, b, ob, brs, bcs, bpt, c, oc,
+                             crs, ccs, cpt, batch, apt2, bpt2, cpt2, batch2)
     lib = _lib.load()
     if host:
         if str(da) not in ("float32", "float64"):

@@ -588,10 +588,19 @@ def _execute_conventional(plan, a, b, alpha, beta, c, counters):
 
 
 def _storage_overlap(x, y) -> bool:
+    """Whether the memory spans of two tensors intersect (for strided views the
+    span from the lowest to the highest addressed element)."""
     if x.device != y.device:
         return False
-    xs, ys = x.data_ptr(), y.data_ptr()
-    xe, ye = xs + x.numel() * x.element_size(), ys + y.numel() * y.element_size()
+
+    def span(t):
+        lo = t.data_ptr()
+        if t.numel() == 0:
+            return lo, lo
+        top = sum((d - 1) * s for d, s in zip(t.shape, t.stride()) if d > 0)
+        return lo, lo + (top + 1) * t.element_size()
+    xs, xe = span(x)
+    ys, ye = span(y)
     return xs < ye and ys < xe
 
 
@@ -645,6 +654,7 @@ def execute_plans(calls) -> None:
     import torch
 
     from . import _lib
+    from . import kernels as _k
     calls = list(calls)
     if not calls:
         return
@@ -671,6 +681,10 @@ def execute_plans(calls) -> None:
         x, y = (a.data, b.data) if L.first == "A" else (b.data, a.data)
         ars, acs, apt, apt2, brs, bcs, bpt, bpt2, crs, ccs, cpt, cpt2 = L.strides
         for ox, oy, oc in L.outer:
+            if L.batch == 0 or L.batch2 == 0:
+                continue
+            _k.validate_call(L.m, L.n, L.k, x, ox, ars, acs, apt, y, oy, brs, bcs, bpt,
+                             c.data, oc, crs, ccs, cpt, L.batch, apt2, bpt2, cpt2, L.batch2)
             descs.append(_lib.GemmDesc(L.m, L.n, L.k, float(alpha), float(beta),
                                        x.data_ptr(), ox, ars, acs, apt, apt2,
                                        y.data_ptr(), oy, brs, bcs, bpt, bpt2,
@@ -683,6 +697,8 @@ def execute_plans(calls) -> None:
                            _storage_overlap(ci, bj)):
                 raise ValueError(f"grouped calls {i} and {j} are not independent "
                                  "(a C overlaps another call's operands)")
+    if not descs:
+        return
     arr = (_lib.GemmDesc * len(descs))(*descs)
     lib = _lib.load()
     fn = lib.sbt_batched_core_group_f64 if dtype == torch.float64 else \

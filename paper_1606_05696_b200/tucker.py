@@ -346,7 +346,7 @@ def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
             qt = _orthonormal(yt)
     u = ut.t()
     if ut32 is not None:
-        u._sbt_f32 = ut32          # fp32 copy for the fp32 mode products
+        _attach_f32(u, ut32)       # fp32 copy for the fp32 mode products
     return u
 
 
@@ -358,7 +358,7 @@ def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
     labels_a = tuple("k" if i == r else _LETTERS[i] for i in range(order))
     labels_c = tuple("z" if i == r else _LETTERS[i] for i in range(order))
     spec = ContractionSpec(labels_a, labels_b, labels_c)
-    b = _as_factor_tensor(u, cur.dtype)
+    b = _as_factor_tensor(u, cur.dtype, cur.data.device)
     dims = list(cur.layout.dims)
     dims[r] = out_ext
     out = DenseTensor.empty(Layout.packed(dims), dtype=cur.dtype, device=cur.device)
@@ -386,18 +386,33 @@ def _planned(spec, la, lb, lc):
     return plan
 
 
-def _as_factor_tensor(u, dtype):
-    """Factor matrix (dim x rank, logical) as a packed column-major DenseTensor.
-    The fp32 conversion is made once per factor and kept on the tensor (the
-    device Ritz kernel supplies it directly)."""
+def _attach_f32(u, flat):
+    """Keep an fp32 copy (rank x dim, contiguous) of factor ``u`` on the tensor,
+    stamped with u's version counter: an in-place change of ``u`` (or of the
+    tensor it views) bumps the counter and invalidates the copy."""
+    u._sbt_f32 = (u._version, flat)
+
+
+def _cached_f32(u):
+    got = getattr(u, "_sbt_f32", None)
+    if got is None or got[0] != u._version:
+        return None
+    return got[1]
+
+
+def _as_factor_tensor(u, dtype, device=None):
+    """Factor matrix (dim x rank, logical) as a packed column-major DenseTensor
+    on ``device`` (numpy factors -- the reference's TuckerModel.factors type --
+    are copied there).  The fp32 conversion is made once per factor version
+    and kept on the tensor (the device Ritz kernel supplies it directly)."""
     torch = _torch()
-    u = torch.as_tensor(u)
+    u = torch.as_tensor(u, device=device)
     if dtype == torch.float32:
-        flat = getattr(u, "_sbt_f32", None)
+        flat = _cached_f32(u)
         if flat is None:
             flat = u.to(dtype).t().contiguous()
             if u.is_cuda:
-                u._sbt_f32 = flat
+                _attach_f32(u, flat)
         return DenseTensor(Layout.packed(tuple(u.shape)), flat.reshape(-1))
     flat = u.to(dtype).t().contiguous().reshape(-1)
     return DenseTensor(Layout.packed(tuple(u.shape)), flat)
@@ -499,7 +514,7 @@ class _IterationGraph:
         for u, u32 in zip(self.sets[k], self.sets32[k]):
             v = u.t()
             if u32 is not None:
-                v._sbt_f32 = u32
+                _attach_f32(v, u32)
             vs.append(v)
         return vs
 

@@ -35,6 +35,21 @@
 // contractions (e.g. the 36-case sweep) shares one pipeline fill, one drain
 // and one tile-quantisation tail instead of paying them per contraction.
 //
+// Unbiased narrow tiles (FLUSH: BNT <= 64 with split accumulators, the
+// HBM-bound rank-r products of Tucker/HOOI).  Two biases of the default path
+// matter when such products are chained and their norms compared (the HOOI
+// fit, reference tucker.py:164-167): (1) the raw tile used as hi is x
+// truncated, so the residual that the tensor core truncates again is always of
+// x's sign -- every operand is shrunk by ~2^-22 on average; (2) the main
+// accumulator is truncated on every MMA, a shrink of ~K/16 ulp for coherent
+// sums.  FLUSH removes both: the converters write hi = rna_tf32(x) in place
+// and lo = rna_tf32(x - hi) (signs now independent of x), and the hi*hi MMA of
+// every group of G K=8 steps writes a FRESH TMEM step accumulator (8 rotating
+// slots) that the epilogue warps add into registers in round-to-nearest fp32,
+// in k order; the 2^-11-sized cross terms keep their own accumulator.  The
+// tiles are HBM-paced (~700 cycles per K-block), so the extra TMEM loads and
+// adds are hidden.
+//
 // Batch-blocked A (BB, the exceptional cases, reference kernels.py:179-204):
 // the A operand is unit-stride along the BATCH mode (apt = 1) while C is
 // unit-stride along m.  Each CTA's 128 MMA rows are (4 consecutive batch
@@ -208,6 +223,17 @@ __device__ __forceinline__ void tma_operand(bool kmaj, const CUtensorMap* tm, ui
   }
 }
 
+// FLUSH configuration (see the header): step-accumulator slots after the
+// NBUF x ACC_W accumulator columns
+template <bool SPLIT_ACC, bool BB, int BNT>
+struct FlushCfg {
+  static constexpr bool ON = SPLIT_ACC && !BB && BNT <= 64;
+  static constexpr int ACC_W = (SPLIT_ACC ? 2 : 1) * BNT;
+  static constexpr int NBUF = 512 / ACC_W >= 2 ? 2 : 1;
+  static constexpr int BASE = NBUF * ACC_W;
+  static constexpr int NSLOT = ON ? ((512 - BASE) / BNT < 8 ? (512 - BASE) / BNT : 8) : 1;
+};
+
 template <int MAXP, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256, int EPIB = 2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefetch) {
@@ -237,7 +263,15 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
   uint64_t* lo_empty = full + RAW_SLOTS;
   uint64_t* acc_full = lo_empty + LO_SLOTS;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  using FC = FlushCfg<SPLIT_ACC, BB, BNT>;
+  constexpr bool FLUSH = FC::ON;
+  constexpr int NSLOT = FC::NSLOT;
+  uint64_t* step_full = acc_empty + 2;           // FLUSH step accumulators
+  uint64_t* step_empty = step_full + NSLOT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(step_empty + NSLOT);
+  static_assert((3 * RAW_SLOTS + LO_SLOTS + 4 + 2 * NSLOT) * 8 + 4 <= 512, "barrier area");
+  // FLUSH: K=8 steps per step-accumulator group (1, 2 or 4; log2 in bits 12-13)
+  const int flush_lg = (p_prefetch >> 12) & 3;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -260,6 +294,10 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       for (int b = 0; b < 2; ++b) {
         ptx::mbar_init(&acc_full[b], 1);
         ptx::mbar_init(&acc_empty[b], 2 * 4);  // one arrival per epilogue warp of each CTA
+      }
+      for (int s = 0; s < NSLOT; ++s) {
+        ptx::mbar_init(&step_full[s], 1);
+        ptx::mbar_init(&step_empty[s], 2 * 4);
       }
       ptx::fence_mbarrier_init();
       for (int i = 0; i < nprob; ++i) {
@@ -432,10 +470,20 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
             ptx::sts_v4(lo_base + Gm::SLOT_BYTES + off, __float_as_uint(v[i].x),
                         __float_as_uint(v[i].y), __float_as_uint(v[i].z), __float_as_uint(v[i].w));
           }
-          ptx::sts_v4(lo_base + off, __float_as_uint(ptx::tf32_residual(v[i].x)),
-                      __float_as_uint(ptx::tf32_residual(v[i].y)),
-                      __float_as_uint(ptx::tf32_residual(v[i].z)),
-                      __float_as_uint(ptx::tf32_residual(v[i].w)));
+          if constexpr (FLUSH) {  // unbiased split, hi written back in place
+            uint32_t h[4], l[4];
+            ptx::split_tf32(v[i].x, h[0], l[0]);
+            ptx::split_tf32(v[i].y, h[1], l[1]);
+            ptx::split_tf32(v[i].z, h[2], l[2]);
+            ptx::split_tf32(v[i].w, h[3], l[3]);
+            ptx::sts_v4(raw + off, h[0], h[1], h[2], h[3]);
+            ptx::sts_v4(lo_base + off, l[0], l[1], l[2], l[3]);
+          } else {
+            ptx::sts_v4(lo_base + off, __float_as_uint(ptx::tf32_residual(v[i].x)),
+                        __float_as_uint(ptx::tf32_residual(v[i].y)),
+                        __float_as_uint(ptx::tf32_residual(v[i].z)),
+                        __float_as_uint(ptx::tf32_residual(v[i].w)));
+          }
         }
       }
       ptx::fence_proxy_async_smem();
@@ -453,12 +501,53 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     const int r = warp * 32 + lane;
     const bool leader = (r == 0);
     uint32_t nchunk = 0, tcount = 0;
+    uint32_t eg = 0;  // FLUSH: step-accumulator groups consumed (all tiles)
+    const uint32_t step_empty_leader = FLUSH ? ptx::mapa(&step_empty[0], 0) : 0u;
     int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
       const Problem& P = prob(t, cur);
       const GemmParams<float>& p = P.p;
       const Fold& f = P.f;
       const Tile tc = tile_of<BB, BNT>(t - P.tile_begin, P.tiles_m, P.tiles_n, P.nbatch);
+      // FLUSH: sum the tile's hi*hi step accumulators in round-to-nearest fp32
+      // (k order), then park the sum in the tile's main accumulator columns,
+      // which the MMAs do not write in this mode
+      float facc[FLUSH ? BNT : 1];
+      if constexpr (FLUSH) {
+#pragma unroll
+        for (int j = 0; j < BNT; ++j) facc[j] = 0.f;
+        const uint32_t ngroups = uint32_t(P.nkb * (BK / 8)) >> flush_lg;
+#pragma unroll 1
+        for (uint32_t gi = 0; gi < ngroups; ++gi, ++eg) {
+          const uint32_t slot = eg % NSLOT;
+          ptx::mbar_wait(&step_full[slot], (eg / NSLOT) & 1u);
+          ptx::tc_fence_after();
+          uint32_t v[BNT];
+#pragma unroll
+          for (int c = 0; c < BNT; c += 16)
+            ptx::tmem_ld16(tmem + lane_addr + FC::BASE + slot * BNT + c,
+                           *reinterpret_cast<uint32_t(*)[16]>(v + c));
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (rank == 0) ptx::mbar_arrive(&step_empty[slot]);
+            else ptx::mbar_arrive_remote(step_empty_leader + slot * 8);
+          }
+#pragma unroll
+          for (int j = 0; j < BNT; ++j) facc[j] += __uint_as_float(v[j]);
+        }
+      }
+      auto park_flush = [&](uint32_t acc_col) {
+        if constexpr (FLUSH) {
+#pragma unroll
+          for (int c = 0; c < BNT; c += 16)
+            ptx::tmem_st16(tmem + lane_addr + acc_col + c,
+                           *reinterpret_cast<const uint32_t(*)[16]>(
+                               reinterpret_cast<const uint32_t*>(facc) + c));
+          ptx::tmem_st_wait();
+        }
+      };
     if (!BB && f.cmode) {
       // TMA-store epilogue: per 32-column chunk, TMEM -> registers (alpha) ->
       // per-warp smem staging (EPIB buffers) -> one TMA store of a 32 x 32 box
@@ -472,6 +561,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
 #endif
         ptx::mbar_wait(&acc_full[b], ph);
         ptx::tc_fence_after();
+        park_flush(b * ACC_W);
 #ifdef SBT_TRACE
         const long long tt1 = clock64();
         long long tt2 = 0, ph_ld = 0, ph_bw = 0, ph_st = 0;
@@ -598,6 +688,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       const uint32_t ph = NBUF == 2 ? ((tcount >> 1) & 1u) : (tcount & 1u);
       ptx::mbar_wait(&acc_full[b], ph);
       ptx::tc_fence_after();
+      park_flush(b * ACC_W);
 #ifdef SBT_TRACE
       long long t_ld = 0, t_begin = clock64();
 #endif
@@ -696,6 +787,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     // SBO 512 (4-row K groups), K=8 step = 1024 B.
     constexpr uint32_t k_lay = BK == 32 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
     uint32_t it = 0, tcount = 0;
+    uint32_t u = 0;  // FLUSH: K=8 steps issued (all tiles)
     int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
       const Problem& P = prob(t, cur);
@@ -727,7 +819,32 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
         const uint32_t b_lo = a_lo + Gm::A_BYTES;
         // BB: A_hi is the converter's swizzled copy, not the dense raw box
         const uint32_t a_raw = BB ? a_lo + Gm::SLOT_BYTES : b_raw - Gm::A_BYTES;
-        if (ptx::elect_one_sync()) {
+        if constexpr (FLUSH) {
+          const uint32_t gmask = (1u << flush_lg) - 1u;
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j, ++u) {
+            const uint32_t grp = u >> flush_lg, slot = grp % NSLOT, within = u & gmask;
+            if (within == 0) {  // the epilogue drained this slot's previous group
+              ptx::mbar_wait(&step_empty[slot], ((grp / NSLOT) & 1u) ^ 1u);
+              ptx::tc_fence_after();
+            }
+            if (ptx::elect_one_sync()) {
+              const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t dbr = ptx::umma_desc(b_raw + j * b_step, b_lbo, b_sbo, b_lay);
+              const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
+              ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, (kb | j) ? 1u : 0u);
+              ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
+              ptx::mma2_tf32_ss(tmem + FC::BASE + slot * BNT, dar, dbr, idesc, within ? 1u : 0u);
+              if (within == gmask) ptx::tc_commit2_mc(&step_full[slot], 0x3);
+              if (j == BK / 8 - 1) {
+                ptx::tc_commit2_mc(&raw_empty[s], 0x3);
+                ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
+              }
+            }
+            __syncwarp();
+          }
+        } else if (ptx::elect_one_sync()) {
 #pragma unroll
           for (int j = 0; j < BK / 8; ++j) {
             const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);

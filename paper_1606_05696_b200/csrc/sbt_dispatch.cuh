@@ -188,11 +188,12 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
     const tf32tma::Fold f =
         variant == 6 ? tf32tma::Fold{q.m, q.n, q.m, q.n, 0, 0, 0} : make_fold(q, qa == 2);
     // narrow N (< 96) only pays off for many M rows in total (HBM-bound skinny
-    // products: rank-r Tucker mode products); narrow tiles need K-major B
+    // products: rank-r Tucker mode products, any rank -- the unbiased FLUSH
+    // mode runs there); narrow tiles need K-major B
     const int64_t rows = f.mtot * ((f.fm == 1 || f.fn == 1) ? 1 : q.batch) *
                          ((f.fm == 2 || f.fn == 2) ? 1 : q.batch2);
     const bool ok = variant == 4 ||
-                    (f.mtot >= 256 && (f.ntot >= 96 || (f.ntot >= 16 && rows >= 8192 && qb == 1)));
+                    (f.mtot >= 256 && (f.ntot >= 96 || (rows >= 8192 && qb == 1)));
     // ties: prefer C unit-stride along N (vector staging stores in the
     // TMA-store epilogue: 8 x 16 B per thread and chunk instead of 32 x 4 B)
     static const int prefer_rowmajor_c = env_int("SBT_TC_PREFER_CN", 1);
@@ -209,6 +210,10 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
   if (out->bnt < 64 && out->bm != 1) return false;  // 16-column B halves must be K-major
   out->bb = false;
   out->split = pick_split(out->p);
+  // narrow tiles run the unbiased FLUSH mode (k_tf32x3_pair_tma.cuh header),
+  // which keeps the cross terms in the split accumulator
+  static const int narrow_flush = env_int("SBT_TC_FLUSH", 1);
+  if (narrow_flush && out->bnt <= 64) out->split = true;
   // split accumulators (K > 512) fill TMEM at 256 columns: 128-wide tiles keep
   // them double-buffered, so the epilogue overlaps the next tile's MMAs
   static const int split_bnt = env_int("SBT_TC_SPLIT_BNT", 256);
@@ -277,7 +282,11 @@ static int launch_pair_set(const tf32tma::ProblemSet<MAXP>& ps, cudaStream_t str
   const int64_t pairs = ps.total < kNumSMs / 2 ? ps.total : kNumSMs / 2;
   // low byte: L2 prefetch distance (measured: no gain, 0); bits 8/9: diagnostics
   // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
-  static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8);
+  // bits 12-13: log2 of the K=8 steps per FLUSH step-accumulator group
+  // (SBT_TC_FLUSH_G = 1 / 2 / 4; narrow tiles only)
+  static const int flush_g = env_int("SBT_TC_FLUSH_G", 1);
+  static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8) |
+                              ((flush_g >= 4 ? 2 : flush_g >= 2 ? 1 : 0) << 12);
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(ps, prefetch);
   note_launch(name);
   return 1;

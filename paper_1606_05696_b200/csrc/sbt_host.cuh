@@ -104,6 +104,8 @@ struct HostCtx {
   size_t arena_bytes = 0;
   void* slot[kSlots] = {};
   cudaEvent_t ev[kSlots] = {};
+  uint32_t next_slot = 0;  // staging slots rotate across calls: a slot is
+                           // refilled only after its last copy drained
   bool ok = false;
 
   explicit HostCtx(int dev) : device(dev) {
@@ -160,11 +162,13 @@ inline cudaError_t upload(HostCtx* cx, void* dst, const void* src, size_t bytes)
   if (bytes == 0) return cudaSuccess;
   if (is_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cx->stream);
   cudaError_t e = cudaSuccess;
-  int i = 0;
-  for (size_t off = 0; off < bytes; off += kSlotBytes, ++i) {
-    const int s = i % kSlots;
+  for (size_t off = 0; off < bytes; off += kSlotBytes) {
+    // the slot's previous H2D copy (this call or an earlier upload of the same
+    // call sequence, e.g. A before B) must have read it before the host
+    // overwrites it; an event never recorded completes immediately
+    const int s = int(cx->next_slot++ % kSlots);
     const size_t len = bytes - off < kSlotBytes ? bytes - off : kSlotBytes;
-    if (i >= kSlots && (e = cudaEventSynchronize(cx->ev[s])) != cudaSuccess) return e;
+    if ((e = cudaEventSynchronize(cx->ev[s])) != cudaSuccess) return e;
     CopyPool::get().copy(cx->slot[s], static_cast<const char*>(src) + off, len);
     if ((e = cudaMemcpyAsync(static_cast<char*>(dst) + off, cx->slot[s], len,
                              cudaMemcpyHostToDevice, cx->stream)) != cudaSuccess)

@@ -289,13 +289,6 @@ def test_36_cases_square_vs_oracle(n, dtype):
         assert err <= TOL[dtype], (case.case_id, n, err)
 
 
-@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
-@pytest.mark.parametrize("cid", ["1.1", "1.3", "2.4", "3.4", "5.5", "6.4", "6.6"])
-def test_selected_cases_n256_vs_oracle(cid, dtype):
-    err = _case_run(cid, 256, dtype, seed=hash(cid) % 1000)
-    assert err <= TOL[dtype], (cid, err)
-
-
 @pytest.mark.parametrize("which", ["generic", "auto"])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_kernel_families_agree_on_odd_and_aligned_shapes(which, dtype):
@@ -596,15 +589,15 @@ def test_hooi_subspace_path_matches_oracle():
     core = rng.standard_normal(ranks)
     us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
     full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
-    # fp32: fit = 1 - sqrt(|T|^2 - |G|^2)/|T| amplifies a relative error e in
-    # |G|^2 by |G|^2 / (2 |T| resid) (~5x here, resid/|T| = 0.09); the 3xTF32
-    # products carry e ~ 4e-6 (the tensor core truncates its fp32 accumulator
-    # once per K=8 MMA), so the fp32 fit is checked to 5e-5 absolute.
-    for dtype, fatol, utol in (("float64", 1e-10, 1e-8), ("float32", 5e-5, 1e-4)):
+    # fp32: the rank products run the unbiased narrow-tile mode (round-to-
+    # nearest TF32 split, step accumulators summed in RN fp32), so the fit
+    # -- which amplifies a relative bias e in |G|^2 by |G|^2 / (2 |T| resid) --
+    # meets the north_star fp32 tolerance, rel 1e-5
+    for dtype, frtol, utol in (("float64", 1e-10, 1e-8), ("float32", 1e-5, 1e-4)):
         t = DenseTensor.from_array(full, dtype=dtype)
         model = sbt.hooi(t, ranks, max_iters=3, tol=-1.0)
         ref = otucker.hooi(t.to_array().astype(np.float64), ranks, max_iters=3, tol=-1.0)
-        np.testing.assert_allclose(model.fit_history, ref["fit_history"], rtol=0, atol=fatol)
+        np.testing.assert_allclose(model.fit_history, ref["fit_history"], rtol=frtol, atol=0)
         for r in range(3):
             u = model.factors[r].cpu().numpy()
             ur = ref["factors"][r]

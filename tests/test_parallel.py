@@ -118,3 +118,56 @@ def test_hooi_sharded_two_ranks_matches_oracle(dims):
     np.testing.assert_allclose(r0["fits"], ref["fit_history"], atol=1e-10)
     for u, ur in zip(r0["u"], ref["factors"]):
         np.testing.assert_allclose(u @ u.T, ur @ ur.T, atol=1e-8)
+
+
+def _slab_worker(rank, world, cid, ext, seed):
+    """Rank r evaluates its slab of one contraction (shard_contraction views
+    into the full buffers, the reference planner lowering on the host) and the
+    slabs are all-gathered; no collective on the data path itself."""
+    from oracle import plan as oplan
+    rng = np.random.default_rng(seed)
+    case = [c for c in enumerate_cases(2, 3) if c.case_id == cid][0]
+    spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+    la, lb, lc = (Layout.packed([ext[l] for l in labs])
+                  for labs in (spec.labels_a, spec.labels_b, spec.labels_c))
+    A, B = rng.standard_normal(la.size), rng.standard_normal(lb.size)
+    C = np.zeros(lc.size)
+    sh = shard_contraction(spec, la, lb, lc, world, rank)
+    sla, slb, slc = sh.layouts
+    local_ext = dict(ext)
+    local_ext[sh.label] = sh.stop - sh.start
+    oplan.contract(spec.labels_a, spec.labels_b, spec.labels_c, local_ext,
+                   A[sh.offsets[0]:], B[sh.offsets[1]:], 1.0, 0.0, C[sh.offsets[2]:],
+                   layouts=(sla, slb, slc))
+    mine = torch.tensor(C)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    got = sum(p.numpy() for p in parts)     # slabs are disjoint: the sum reassembles C
+    want = np.zeros(lc.size)
+    oplan.contract(spec.labels_a, spec.labels_b, spec.labels_c, ext, A, B, 1.0, 0.0, want)
+    return float(np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("cid", ["1.1", "1.3", "3.4", "5.2", "6.6"])
+def test_shard_contraction_two_processes(cid):
+    """world_size 2 (gloo): each rank executes only its slab; the gathered
+    slabs equal the full contraction."""
+    ext = dict(m=6, n=5, p=9, k=4)
+    out = _run(2, _slab_worker, cid, ext, 5)
+    assert all(err <= 1e-12 for _, err in out), out
+
+
+def test_bench_spawns_ranks():
+    """bench.py --gpus N outside torchrun starts N ranks itself (the reference
+    arm runs on rank 0 only and reports n_gpus = N)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--n", "16"],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"

@@ -32,6 +32,7 @@
 #ifndef SBT200_H
 #define SBT200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -80,6 +81,34 @@ int sbt_probe_tf32_sustained(double seconds, double* tflops);
 int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, double tol,
                  double* ut, double* yt, float* ut32, double* w, int* flag, double* rel,
                  void* stream);
+
+/* ---- reference: tucker.py:63-76 applied at tucker.py:160-167 (one warm
+        HOOI factor update, device-finished).  y: a packed column-major
+        tensor of `order` extents `dims` (fp32 or fp64 elements); n =
+        dims[mode].  qt: the previous factor's p columns as rows of ldq
+        doubles (p <= 64).  Forms Z = Y_(mode) Y_(mode)^T Q in fp64 straight
+        from y (no unfolding copy; fp32 widened on load; deterministic) in the
+        caller's workspace `ws` (sbt_hooi_factor_ws_bytes bytes, zero-filled
+        once before its first use; the library leaves it reusable), then
+        finishes the sweep exactly as sbt_ritz_f64 with m = NULL.  Three
+        launches, no host synchronisation, capturable. */
+size_t sbt_hooi_factor_ws_bytes(int order, const int64_t* dims, int mode, int p);
+int sbt_hooi_factor_f32(const float* y, int order, const int64_t* dims, int mode,
+                        const double* qt, int64_t ldq, int p, int rank, double tol, void* ws,
+                        size_t ws_bytes, double* ut, double* yt, float* ut32, double* w,
+                        int* flag, double* rel, void* stream);
+int sbt_hooi_factor_f64(const double* y, int order, const int64_t* dims, int mode,
+                        const double* qt, int64_t ldq, int p, int rank, double tol, void* ws,
+                        size_t ws_bytes, double* ut, double* yt, float* ut32, double* w,
+                        int* flag, double* rel, void* stream);
+/* ---- reference: tucker.py:164-168 (fit from ||G||).  out[0] = ||core||_2
+        (fp64 sum of squares over `count` packed elements, fixed order),
+        out[1 + f] = flags[f] for f < nflags (<= 64): the HOOI iteration's one
+        device->host read. */
+int sbt_hooi_status_f32(const float* core, int64_t count, const int* flags, int nflags,
+                        double* out, void* stream);
+int sbt_hooi_status_f64(const double* core, int64_t count, const int* flags, int nflags,
+                        double* out, void* stream);
 
 /* ---- reference: layout.py:202-215 permute_copy (the conventional strategy's
         explicit transposition, planner.py:620-713; NOT used by planned

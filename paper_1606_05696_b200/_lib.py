@@ -69,6 +69,13 @@ SIGNATURES = {
                         c_int),
     "sbt_ritz_f64": ([_P, _P, c_int64, c_int, c_int, c_double, _P, _P, _P, _P, _P, _P, _P],
                      c_int),
+    "sbt_hooi_factor_ws_bytes": ([c_int, ctypes.POINTER(c_int64), c_int, c_int], ctypes.c_size_t),
+    "sbt_hooi_factor_f32": ([_P, c_int, ctypes.POINTER(c_int64), c_int, _P, c_int64, c_int, c_int,
+                             c_double, _P, ctypes.c_size_t, _P, _P, _P, _P, _P, _P, _P], c_int),
+    "sbt_hooi_factor_f64": ([_P, c_int, ctypes.POINTER(c_int64), c_int, _P, c_int64, c_int, c_int,
+                             c_double, _P, ctypes.c_size_t, _P, _P, _P, _P, _P, _P, _P], c_int),
+    "sbt_hooi_status_f32": ([_P, c_int64, _P, c_int, _P, _P], c_int),
+    "sbt_hooi_status_f64": ([_P, c_int64, _P, c_int, _P, _P], c_int),
     "sbt_batched_core_group_f32": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),
     "sbt_batched_core_group_f64": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),
     "sbt_gemm_core_f64": (_core_sig(c_double), c_int),

@@ -80,7 +80,8 @@ __device__ __forceinline__ void small_mm(const double* X, const double* Y, doubl
   }
 }
 
-// qz: [Q | Z] stored as 2p rows of length n (row j = column j of Q, then of Z);
+// q / z: the columns of Q and of Z = G Q as p rows each (row j at q + j * ldq,
+// z + j * ldz; the entry point's qz = [Q | Z] is q = qz, z = qz + p * n);
 // m: the (2p x p) column-major product [Q Z]^T Z (ld 2p).
 // m == nullptr: H = Q^T Z is formed in-kernel.
 // ut: rank rows of length n (U column-major); yt (optional): the same for
@@ -90,7 +91,8 @@ __device__ __forceinline__ void small_mm(const double* X, const double* Y, doubl
 // rel[1] = Jacobi sweeps, rel[2..4] = SM cycles of the eigen / Ritz-vector /
 // sign phases, rel[5] = Newton refinement steps (diagnostics).
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kThreads, 1)
-ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t n, int p,
+ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict__ z,
+            int64_t ldz, const double* __restrict__ m, int64_t n, int p,
             int rank, double tol, double* __restrict__ ut, double* __restrict__ yt,
             float* __restrict__ ut32, double* __restrict__ w, int* __restrict__ flag,
             double* __restrict__ rel) {
@@ -132,8 +134,8 @@ ritz_kernel(const double* __restrict__ qz, const double* __restrict__ m, int64_t
     for (int e = tid; e < p * kTileRows; e += kThreads) {
       const int l = e / kTileRows, rr = e % kTileRows;
       const bool in = rr < rows;
-      Qs[l * LDT + rr] = in ? qz[int64_t(l) * n + i0 + rr] : 0.0;
-      Zs[l * LDT + rr] = in ? qz[int64_t(p + l) * n + i0 + rr] : 0.0;
+      Qs[l * LDT + rr] = in ? q[int64_t(l) * ldq + i0 + rr] : 0.0;
+      Zs[l * LDT + rr] = in ? z[int64_t(l) * ldz + i0 + rr] : 0.0;
     }
   };
   // m == nullptr: H = Q^T Z from the cluster's row tiles (partial per CTA in

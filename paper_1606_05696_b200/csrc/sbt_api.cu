@@ -25,6 +25,7 @@
 #include "k_probe.cuh"
 #include "k_permute.cuh"
 #include "k_ritz.cuh"
+#include "k_gram_apply.cuh"
 
 namespace sbt {
 
@@ -545,9 +546,113 @@ int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, 
     if (rc != SBT_OK) return rc;
   }
   ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-      qz, m, n, p, rank, tol, ut, yt, ut32, w, flag, rel);
+      qz, n, qz + int64_t(p) * n, n, m, n, p, rank, tol, ut, yt, ut32, w, flag, rel);
   note_launch("ritz");
   return check_cuda(cudaGetLastError(), "ritz launch");
+}
+
+}  // extern "C"
+
+namespace {
+
+// the unfolding geometry of a packed tensor (k_gram_apply.cuh)
+int unfold_of(int order, const int64_t* dims, int mode, sbt::gapply::Unfold& u) {
+  if (order < 1 || order > 16 || !dims || mode < 0 || mode >= order) return -1;
+  int64_t a = 1, total = 1;
+  for (int i = 0; i < order; ++i) {
+    if (dims[i] < 1) return -1;
+    if (i < mode) a *= dims[i];
+    total *= dims[i];
+  }
+  u.n = dims[mode];
+  u.cols = total / u.n;
+  u.A = a;
+  return 0;
+}
+
+template <typename TY>
+int hooi_factor(const TY* y, int order, const int64_t* dims, int mode, const double* qt,
+                int64_t ldq, int p, int rank, double tol, void* ws, size_t ws_bytes, double* ut,
+                double* yt, float* ut32, double* w, int* flag, double* rel, void* stream_) {
+  using namespace sbt;
+  gapply::Unfold u;
+  if (!y || !qt || !ws || !ut || !w || !flag || !rel || unfold_of(order, dims, mode, u) ||
+      p < 1 || p > gapply::kMaxP || p > ritz::kMaxP || rank < 1 || rank > p || p > u.n ||
+      ldq < u.n)
+    return fail(SBT_EINVAL, "sbt_hooi_factor: bad arguments");
+  const gapply::Plan pl = gapply::plan(u.n, u.cols, p);
+  if (ws_bytes < size_t(pl.bytes))
+    return fail(SBT_EINVAL, "sbt_hooi_factor: workspace too small (see sbt_hooi_factor_ws_bytes)");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  double* wsd = static_cast<double*>(ws);
+  double* wt = wsd + pl.w_off;
+  double* part = wsd + pl.part_off;
+  double* zt = wsd + pl.z_off;
+  unsigned* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + pl.cnt_off_bytes);
+  gapply::w_kernel<TY><<<unsigned(ceil_div(u.cols, gapply::CB)), gapply::NT, 0, stream>>>(
+      y, u, qt, ldq, p, wt);
+  note_launch("gram_apply_w");
+  int rc = check_cuda(cudaGetLastError(), "gram_apply_w launch");
+  if (rc != SBT_OK) return rc;
+  gapply::z_kernel<TY><<<dim3(unsigned(pl.tiles), unsigned(pl.splits)), gapply::NT, 0, stream>>>(
+      y, u, wt, p, pl.kper, zt, u.n, part, cnt);
+  note_launch("gram_apply_z");
+  rc = check_cuda(cudaGetLastError(), "gram_apply_z launch");
+  if (rc != SBT_OK) return rc;
+  rc = set_smem_attr(reinterpret_cast<const void*>(ritz::ritz_kernel), ritz::SMEM_BYTES);
+  if (rc != SBT_OK) return rc;
+  ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, stream>>>(
+      qt, ldq, zt, u.n, nullptr, u.n, p, rank, tol, ut, yt, ut32, w, flag, rel);
+  note_launch("ritz");
+  return check_cuda(cudaGetLastError(), "ritz launch");
+}
+
+template <typename T>
+int hooi_status(const T* x, int64_t count, const int* flags, int nflags, double* out,
+                void* stream) {
+  using namespace sbt;
+  if (!x || count < 0 || nflags < 0 || nflags > 64 || (nflags && !flags) || !out)
+    return fail(SBT_EINVAL, "sbt_hooi_status: bad arguments");
+  gapply::status_kernel<T><<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(x, count, flags,
+                                                                              nflags, out);
+  note_launch("hooi_status");
+  return check_cuda(cudaGetLastError(), "hooi_status launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sbt_hooi_factor_ws_bytes(int order, const int64_t* dims, int mode, int p) {
+  sbt::gapply::Unfold u;
+  if (unfold_of(order, dims, mode, u) || p < 1 || p > sbt::gapply::kMaxP) return 0;
+  return size_t(sbt::gapply::plan(u.n, u.cols, p).bytes);
+}
+
+int sbt_hooi_factor_f32(const float* y, int order, const int64_t* dims, int mode,
+                        const double* qt, int64_t ldq, int p, int rank, double tol, void* ws,
+                        size_t ws_bytes, double* ut, double* yt, float* ut32, double* w,
+                        int* flag, double* rel, void* stream) {
+  return hooi_factor<float>(y, order, dims, mode, qt, ldq, p, rank, tol, ws, ws_bytes, ut, yt,
+                            ut32, w, flag, rel, stream);
+}
+
+int sbt_hooi_factor_f64(const double* y, int order, const int64_t* dims, int mode,
+                        const double* qt, int64_t ldq, int p, int rank, double tol, void* ws,
+                        size_t ws_bytes, double* ut, double* yt, float* ut32, double* w,
+                        int* flag, double* rel, void* stream) {
+  return hooi_factor<double>(y, order, dims, mode, qt, ldq, p, rank, tol, ws, ws_bytes, ut, yt,
+                             ut32, w, flag, rel, stream);
+}
+
+int sbt_hooi_status_f32(const float* core, int64_t count, const int* flags, int nflags,
+                        double* out, void* stream) {
+  return hooi_status<float>(core, count, flags, nflags, out, stream);
+}
+
+int sbt_hooi_status_f64(const double* core, int64_t count, const int* flags, int nflags,
+                        double* out, void* stream) {
+  return hooi_status<double>(core, count, flags, nflags, out, stream);
 }
 
 }  // extern "C"

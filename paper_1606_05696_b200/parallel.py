@@ -14,13 +14,15 @@ Two regimes, following SURVEY.md section 8e:
   the sharded mode produce partial sums -> all-reduce; products that keep it
   produce a mode-distributed result -> all-gather; norms -> all-reduce.  The
   collectives are NCCL over NVLink on GPU tensors (gloo on CPU tensors in the
-  tests).  The HOSVD initialisation of the sharded mode needs every slab's
-  cross products, so it all-gathers T once.
+  tests).  The HOSVD Gram of the sharded mode needs every slab's cross
+  products: the slabs travel around a ring (two resident at a time), T is
+  never gathered.
 
-Local compute goes through the sm_100a kernels (``paper_1606_05696_b200.tucker``
-mode products).  ``hooi_sharded`` takes an optional ``local`` hook -- the
-tests inject a CPU einsum implementation so the collective logic runs on a
-CPU-only box with gloo; the product path never uses it.
+Local compute goes through the sm_100a kernels (``DeviceOps``: the tucker
+module's mode products, Grams and device-finished factor updates).
+``hooi_sharded`` takes an ``ops`` object -- the tests inject ``HostOps``
+(torch CPU arithmetic) so the collective logic runs on a CPU-only box with
+gloo; the product path never uses it.
 """
 from __future__ import annotations
 
@@ -83,124 +85,247 @@ def shard_contraction(spec: ContractionSpec, la: Layout, lb: Layout, lc: Layout,
 # ----------------------------------------------------------------------------- Tucker
 
 
-def _device_local():
-    """Local kernels: logical torch tensors in, device sm_100a contractions."""
-    from . import tucker as tk
-    from .layout import DenseTensor
+class DeviceOps:
+    """Local work of sharded HOOI on the sm_100a kernels: planned mode
+    products, fp64 Grams on the device, the device-finished factor updates
+    (``sbt_hooi_factor_*``) and the status kernel -- the single-GPU HOOI's
+    own building blocks (``tucker.py``)."""
 
-    def to_dense(x):
+    def __init__(self):
+        from . import tucker as tk
+        self.tk = tk
+
+    def mode_product(self, x, u, mode):
+        return self.tk._mode_product(x, u, mode, True)
+
+    def gram(self, x, r):
+        return self.tk.gram_of_unfolding(x, r)
+
+    def as64(self, x):
         import torch
-        flat = x.permute(*reversed(range(x.dim()))).contiguous().reshape(-1)
-        return DenseTensor(Layout.packed(tuple(x.shape)), flat)
+        return x.data if x.dtype == torch.float64 else x.data.to(torch.float64)
 
-    def from_dense(t):
-        return t.view()
+    def cross_gram(self, xa, ra, xb, rb, k):
+        """Block X_a^T X_b of the last-mode unfolding: xa / xb are (k x ra) /
+        (k x rb) column-major fp64 slabs."""
+        import torch
+        from .kernels import Op, gemm
+        out = torch.empty(ra * rb, dtype=torch.float64, device=xa.device)
+        gemm(Op.Transpose, Op.Normal, ra, rb, k, 1.0, xa, k, xb, k, 0.0, out, ra)
+        return out.reshape(rb, ra).t()
 
-    def mode_product(x, u, mode):
-        return from_dense(tk._mode_product(to_dense(x), u, mode, True))
+    def factor_init(self, g, rank):
+        _, vecs, _ = self.tk.top_eigh(g, rank)
+        return self.tk._sign_fix(vecs.contiguous())
 
-    def gram(x, mode):
-        return tk.gram_of_unfolding(to_dense(x), mode)
+    def factor_iter(self, y, r, rank, warm, status, sweeps):
+        tk = self.tk
+        if tk._ritz_eligible(y.layout.dims[r], rank, warm):
+            return tk._factor_device(y, r, rank, warm, status, r, sweeps)
+        status[r] = 1
+        return tk._factor_from_tensor(y, r, rank, warm=warm)
 
-    return mode_product, gram
+    def factor_host(self, y, r, rank, warm):
+        return self.tk._factor_from_tensor(y, r, rank, warm=warm)
+
+    def new_status(self, order, device):
+        import torch
+        return torch.zeros(order, dtype=torch.int32, device=device)
+
+    def status(self, core, st):
+        import torch
+        out = torch.empty(1 + st.numel(), dtype=torch.float64, device=core.device)
+        return self.tk._hooi_status(core, st, out).cpu().numpy()
+
+    def sumsq(self, x):
+        import torch
+        return torch.sum(x.data.to(torch.float64) ** 2).reshape(1)
 
 
-def _einsum_local():
-    """Reference-free CPU implementation used by the gloo tests only."""
-    import torch
+class HostOps(DeviceOps):
+    """The same steps with torch CPU arithmetic, full eigendecompositions and
+    no device kernels: lets the gloo tests run the sharded driver's
+    collective logic on a CPU-only box.  Never used by the product path."""
 
-    def mode_product(x, u, mode):
-        out = torch.tensordot(u.t().to(x.dtype), x, dims=([1], [mode]))
-        return torch.movedim(out, 0, mode)
+    def __init__(self):
+        from . import tucker as tk
+        self.tk = tk
 
-    def gram(x, mode):
-        m = torch.movedim(x, mode, 0).reshape(x.shape[mode], -1).to(torch.float64)
-        return m @ m.t()
+    def mode_product(self, x, u, mode):
+        import torch
+        from .layout import DenseTensor
+        v = x.view()
+        out = torch.movedim(torch.tensordot(u.t().to(v.dtype), v, dims=([1], [mode])), 0, mode)
+        return DenseTensor.from_array(out, device=x.device)
 
-    return mode_product, gram
+    def gram(self, x, r):
+        import torch
+        v = torch.movedim(x.view(), r, 0).reshape(x.layout.dims[r], -1).to(torch.float64)
+        return v @ v.t()
 
+    def cross_gram(self, xa, ra, xb, rb, k):
+        return xa[:k * ra].reshape(ra, k) @ xb[:k * rb].reshape(rb, k).t()
 
-def _factor(gram, rank, warm=None, dtype="float64"):
-    """Top-``rank`` sign-fixed eigenvectors of an (all-reduced, hence
-    rank-identical) Gram: the device subspace solver for CUDA Grams, the full
-    eigendecomposition for the CPU (gloo test) path."""
-    from .tucker import _SUBSPACE_TOL, _SUBSPACE_TOL_F32, _sign_fix, jacobi_eigh, top_eigh
-    if gram.is_cuda:
-        tol = _SUBSPACE_TOL if dtype == "float64" else _SUBSPACE_TOL_F32
-        _, vecs, _ = top_eigh(gram, rank, q0=warm, tol=tol)
-    else:
-        _, vecs = jacobi_eigh(gram)
-        vecs = vecs[:, :rank]
-    return _sign_fix(vecs.contiguous())
+    def factor_init(self, g, rank):
+        _, vecs = self.tk.jacobi_eigh(g)
+        return self.tk._sign_fix(vecs[:, :rank].contiguous())
+
+    def factor_iter(self, y, r, rank, warm, status, sweeps):
+        status[r] = 1
+        return self.factor_host(y, r, rank, warm)
+
+    def factor_host(self, y, r, rank, warm):
+        return self.factor_init(self.gram(y, r), rank)
+
+    def status(self, core, st):
+        import torch
+        nrm = torch.sqrt(torch.sum(core.data.to(torch.float64) ** 2))
+        return np.concatenate([[float(nrm)], st.to(torch.float64).numpy()])
 
 
 def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e-10,
-                 group=None, local=None):
-    """HOOI with T slab-sharded along its last mode (order 3).
+                 group=None, ops=None):
+    """HOOI with T slab-sharded along its last mode (order 3), reference
+    tucker.py:136-174 with the same products in the same order.
 
-    ``t_local`` is this rank's slab T[:, :, c0:c1] as a logical torch tensor
-    (CUDA for the product path).  Returns (core, factors, fit_history,
-    iterations), identical on every rank.  Same algorithm and product order as
-    ``tucker.hooi`` (reference tucker.py:136-174)."""
+    ``t_local`` is this rank's slab T[:, :, c0:c1] (``slab(d2, world,
+    rank)``) as a packed ``DenseTensor`` (or a logical torch tensor, packed
+    here).  Per mode update: products that contract the sharded mode give
+    partial sums -> all-reduce (r0 d1 r2 / d0 r1 r2 elements); the one that
+    keeps it gives a mode-2-distributed result -> all-gather (r0 r1 d2);
+    ||T||^2 -> all-reduce.  T itself is never gathered: the HOSVD Gram of the
+    sharded mode is assembled from slab cross products passed around a ring
+    (W - 1 point-to-point steps, two slabs resident), then all-gathered as
+    d2 x d2 row blocks.  Factor updates run on the replicated partial cores
+    with the device-finished sweeps (one flag read per iteration; an
+    unconverged factor redoes the iteration on the host-driven path), so every
+    rank holds the same model.  Returns (core as a logical tensor, factors,
+    fit_history, iterations)."""
     import torch
     import torch.distributed as dist
 
+    from .layout import DenseTensor
+
+    ops = ops or DeviceOps()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    d0, d1, d2 = full_dims
+    d0, d1, d2 = (int(d) for d in full_dims)
     c0, c1 = slab(d2, world, rank)
-    if tuple(t_local.shape) != (d0, d1, c1 - c0):
-        raise ValueError(f"rank {rank}: slab shape {tuple(t_local.shape)} != "
-                         f"{(d0, d1, c1 - c0)}")
-    mode_product, gram = local() if local else _device_local()
-    dt = str(t_local.dtype).replace("torch.", "")
+    if isinstance(t_local, torch.Tensor):
+        t_local = DenseTensor.from_array(t_local, device=t_local.device)
+    if tuple(t_local.layout.dims) != (d0, d1, c1 - c0) or not t_local.layout.is_packed():
+        raise ValueError(f"rank {rank}: slab {t_local.layout} != packed {(d0, d1, c1 - c0)}")
     ranks = tuple(int(r) for r in ranks)
+    if len(ranks) != 3 or not all(1 <= r <= d for r, d in zip(ranks, (d0, d1, d2))):
+        raise ValueError(f"invalid ranks {ranks} for dims {full_dims}")
+    dev = t_local.device
+    sizes = [slab(d2, world, r)[1] - slab(d2, world, r)[0] for r in range(world)]
+    starts = [slab(d2, world, r)[0] for r in range(world)]
+    mx = max(sizes)
 
     def allreduce(x):
-        dist.all_reduce(x, group=group)
+        dist.all_reduce(x.data, group=group)
         return x
 
     def allgather_last(x):
-        """Concatenate the ranks' slabs along the last mode (uneven slabs ok)."""
-        sizes = [slab(d2, world, r)[1] - slab(d2, world, r)[0] for r in range(world)]
-        mx = max(sizes)
-        pad = torch.zeros(x.shape[:-1] + (mx,), dtype=x.dtype, device=x.device)
-        pad[..., :x.shape[-1]] = x
+        """Packed (a, b, d2) from the ranks' (a, b, slab) pieces: the last
+        mode is the slowest, so a slab is one contiguous chunk."""
+        a, b, _ = x.layout.dims
+        per = a * b
+        pad = torch.zeros(per * mx, dtype=x.dtype, device=x.device)
+        pad[:x.data.numel()] = x.data
         parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad.contiguous(), group=group)
-        return torch.cat([p[..., :s] for p, s in zip(parts, sizes)], dim=-1)
+        dist.all_gather(parts, pad, group=group)
+        flat = torch.cat([q[:per * s] for q, s in zip(parts, sizes)])
+        return DenseTensor(Layout.packed((a, b, d2)), flat)
 
-    # HOSVD init: modes 0/1 Grams are sums over slabs; the sharded mode needs
-    # the cross-slab products, so gather T once.
+    def ring_gram_last(x):
+        """d2 x d2 Gram of the mode-2 unfolding without gathering T."""
+        k = d0 * d1
+        mine = ops.as64(x)
+        buf = torch.zeros(k * mx, dtype=torch.float64, device=dev)
+        buf[:mine.numel()] = mine
+        rows = torch.zeros(mx, d2, dtype=torch.float64, device=dev)
+        cl = c1 - c0
+        for step in range(world):
+            holder = (rank - step) % world
+            blk = ops.cross_gram(mine, cl, buf, sizes[holder], k)
+            rows[:cl, starts[holder]:starts[holder] + sizes[holder]] = blk
+            if step < world - 1:
+                nbuf = torch.empty_like(buf)
+                reqs = dist.batch_isend_irecv([
+                    dist.P2POp(dist.isend, buf, (rank + 1) % world, group),
+                    dist.P2POp(dist.irecv, nbuf, (rank - 1) % world, group)])
+                for q in reqs:
+                    q.wait()
+                buf = nbuf
+        parts = [torch.empty_like(rows) for _ in range(world)]
+        dist.all_gather(parts, rows, group=group)
+        g = torch.cat([q[:s] for q, s in zip(parts, sizes)])
+        return 0.5 * (g + g.t())
+
+    def local_u2(u2):
+        return u2[c0:c1]
+
+    def chain(factors, skip):
+        """Reference product order (tucker.py:95-99: larger reduction extent
+        first, ties ascending) on the slab; the collective at the end."""
+        modes = sorted((m for m in range(3) if m != skip), key=lambda m: -full_dims[m])
+        cur, partial = t_local, False
+        for m in modes:
+            cur = ops.mode_product(cur, local_u2(factors[m]) if m == 2 else factors[m], m)
+            partial = partial or m == 2
+        return allreduce(cur) if partial else allgather_last(cur)
+
+    # HOSVD initialisation (tucker.py:153-155)
     u = [None, None, None]
     for r in (0, 1):
-        u[r] = _factor(allreduce(gram(t_local, r).contiguous()), ranks[r])
-    t_full = allgather_last(t_local)
-    u[2] = _factor(gram(t_full, 2), ranks[2])
-    del t_full
-    nt2 = allreduce(torch.sum(t_local.to(torch.float64) ** 2).reshape(1))
-    norm_t = float(torch.sqrt(nt2))
-    u2_local = lambda: u[2][c0:c1]  # noqa: E731
+        u[r] = ops.factor_init(allreduce_t(ops.gram(t_local, r).contiguous(), group), ranks[r])
+    u[2] = ops.factor_init(ring_gram_last(t_local), ranks[2])
+    norm_t = float(torch.sqrt(allreduce_t(ops.sumsq(t_local), group)))
+    reuse = d0 >= d1 and d0 >= d2
+
+    def sweep(factors, factor_fn):
+        """One iteration (tucker.py:160-167); returns the core (replicated)."""
+        if reuse:
+            y = chain(factors, 0)
+            factors[0] = factor_fn(y, 0, factors[0])
+            x0 = ops.mode_product(t_local, factors[0], 0)
+            y = allreduce(ops.mode_product(x0, local_u2(factors[2]), 2))
+            factors[1] = factor_fn(y, 1, factors[1])
+            y2 = allgather_last(ops.mode_product(x0, factors[1], 1))
+            factors[2] = factor_fn(y2, 2, factors[2])
+            if d1 >= d2:
+                return ops.mode_product(y2, factors[2], 2)
+            g = allreduce(ops.mode_product(x0, local_u2(factors[2]), 2))
+            return ops.mode_product(g, factors[1], 1)
+        for r in range(3):
+            factors[r] = factor_fn(chain(factors, r), r, factors[r])
+        return chain(factors, None)
 
     fits, prev, iters = [], -np.inf, 0
+    dt = t_local.dtype
     for it in range(max_iters):
         iters = it + 1
-        # skip=0: modes 1 then 2 (contracting the sharded mode: partial sums)
-        y = allreduce(mode_product(mode_product(t_local, u[1], 1), u2_local(), 2).contiguous())
-        u[0] = _factor(gram(y, 0), ranks[0], u[0], dt)
-        x0 = mode_product(t_local, u[0], 0)
-        # skip=1: [0, 2] -> partial sums over the sharded mode
-        y = allreduce(mode_product(x0, u2_local(), 2).contiguous())
-        u[1] = _factor(gram(y, 1), ranks[1], u[1], dt)
-        # skip=2: [0, 1] -> mode-2 distributed result
-        y2 = allgather_last(mode_product(x0, u[1], 1).contiguous())
-        u[2] = _factor(gram(y2, 2), ranks[2], u[2], dt)
-        core = mode_product(y2, u[2], 2)
-        g2 = float(torch.sum(core.to(torch.float64) ** 2))
-        resid = np.sqrt(max(0.0, norm_t ** 2 - g2))
+        sweeps = 2 if (it == 0 or dt == torch.float64) else 1
+        st = ops.new_status(3, dev)
+        start = list(u)
+        core = sweep(u, lambda y, r, warm: ops.factor_iter(y, r, ranks[r], warm, st, sweeps))
+        vals = ops.status(core, st)
+        if not np.all(vals[1:] == 1.0):   # identical on every rank (same inputs, same kernels)
+            u = start
+            core = sweep(u, lambda y, r, warm: ops.factor_host(y, r, ranks[r], warm))
+            vals = ops.status(core, st)
+        resid = np.sqrt(max(0.0, norm_t ** 2 - float(vals[0]) ** 2))
         fit = 1.0 - resid / norm_t if norm_t > 0 else 1.0
         fits.append(fit)
         if fit - prev < tol and it > 0:
             break
         prev = fit
-    return core, u, fits, iters
+    return core.view(), u, fits, iters
+
+
+def allreduce_t(x, group=None):
+    import torch.distributed as dist
+    dist.all_reduce(x, group=group)
+    return x

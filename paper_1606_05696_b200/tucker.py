@@ -196,24 +196,6 @@ def _sign_fix(u):
     return u * signs
 
 
-def _unfolding64(t: DenseTensor, r: int):
-    """fp64 buffer holding the mode-r unfolding Y_(r) column-major with leading
-    dimension dims[r] (mode r first), and its (rows, cols).  An fp64 packed
-    tensor is used in place for r = 0; otherwise one fused pass converts to
-    fp64 and moves mode r first."""
-    torch = _torch()
-    dims = t.layout.dims
-    rows = dims[r]
-    cols = int(np.prod(dims)) // rows
-    if r == 0 and t.dtype == torch.float64 and t.layout.is_packed():
-        return t.data, rows, cols
-    x = t.view().movedim(r, 0)                       # logical (rows, rest...)
-    rev = tuple(reversed(range(x.dim())))
-    buf = torch.empty(tuple(x.shape[i] for i in rev), dtype=torch.float64, device=t.device)
-    buf.copy_(x.permute(rev))                         # column-major, mode r fastest
-    return buf.reshape(-1), rows, cols
-
-
 def gram_of_unfolding(t: DenseTensor, r: int):
     """fp64 Gram matrix Y_(r) Y_(r)^T of the mode-r unfolding, on the device.
 
@@ -297,33 +279,58 @@ def _ritz_eligible(n: int, rank: int, warm) -> bool:
             and 4 * rank <= n and rank <= _RITZ_MAX_P)
 
 
+_FACTOR_WS = {}
+
+
+def _factor_ws(dev, dims, r, p):
+    """Workspace of sbt_hooi_factor for (dims, mode, p): allocated zero-filled
+    once per device and reused (the library leaves it reusable), so a captured
+    iteration allocates nothing."""
+    import ctypes
+    from . import _lib
+    torch = _torch()
+    key = (dev, tuple(dims), r, p)
+    ws = _FACTOR_WS.get(key)
+    if ws is None:
+        d = (ctypes.c_int64 * len(dims))(*dims)
+        nbytes = int(_lib.load().sbt_hooi_factor_ws_bytes(len(dims), d, r, p))
+        if nbytes <= 0:
+            raise ValueError(f"sbt_hooi_factor_ws_bytes: bad geometry {dims} mode {r} p {p}")
+        ws = _FACTOR_WS[key] = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    return ws
+
+
 def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
                    sweeps: int = 1, out=None):
     """Warm-started subspace sweeps on the mode-r Gram, each finished on the
-    device (``sbt_ritz_f64``): sweep 1 on the previous factor, further sweeps
-    on the orthonormalised G U (one sweep reaches the fp32 tolerance after the
-    first HOOI iteration; fp64's 1e-12 takes two).  Writes the last sweep's
+    device: sweep 1 on the previous factor, further sweeps on the
+    orthonormalised G U (one sweep reaches the fp32 tolerance after the first
+    HOOI iteration; fp64's 1e-12 takes two).  A sweep is ONE library call
+    (``sbt_hooi_factor_*``: G Q = Y (Y^T Q) in fp64 read straight from the
+    packed fp32 / fp64 tensor, then the Ritz kernel).  Writes the last sweep's
     convergence flag to status[slot]; never synchronises."""
     import ctypes
     from . import _lib
     torch = _torch()
     fp64 = t.dtype == torch.float64
     tol = _SUBSPACE_TOL if fp64 else _SUBSPACE_TOL_F32
-    # G Q = Y (Y^T Q) from the fp64 unfolding: two rank-p products instead of
-    # the n x n Gram (n^2 * cols flops) and G Q
-    y, n, cols = _unfolding64(t, r)
-    dev = y.device
-    wbuf = torch.empty(rank, cols, device=dev, dtype=torch.float64)  # Y^T Q, col-major
+    if not t.layout.is_packed():
+        t = DenseTensor(Layout.packed(t.layout.dims), t.view().permute(
+            *reversed(range(t.layout.order))).contiguous().reshape(-1))
+    dims = tuple(int(d) for d in t.layout.dims)
+    n = dims[r]
+    dev = t.data.device
     lib = _lib.load()
     ptr = ctypes.c_void_p
     stream = ptr(torch.cuda.current_stream(dev).cuda_stream)
-    qt = torch.as_tensor(warm, device=dev).t()
+    cdims = (ctypes.c_int64 * len(dims))(*dims)
+    entry = lib.sbt_hooi_factor_f64 if fp64 else lib.sbt_hooi_factor_f32
     p = rank
+    ws = _factor_ws(dev, dims, r, p)
+    qt = torch.as_tensor(warm, device=dev).t()          # (p, n) view: row j = column j
+    if qt.stride(1) != 1:
+        qt = qt.contiguous()
     for sweep in range(sweeps):
-        qz = torch.empty(2 * p, n, device=dev, dtype=torch.float64)   # [Q | Z] col-major
-        qz[:p].copy_(qt)
-        _gemm64(Op.Transpose, Op.Normal, cols, p, n, y, n, qz[:p], n, wbuf, cols)  # Y^T Q
-        _gemm64(Op.Normal, Op.Normal, n, p, cols, y, n, wbuf, cols, qz[p:], n)     # Z = Y (Y^T Q)
         last = sweep == sweeps - 1
         if last and out is not None:           # caller-owned (rank x n) buffers
             ut, ut32 = out[0], (out[1] if not fp64 else None)
@@ -335,11 +342,12 @@ def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
         w = torch.empty(rank, device=dev, dtype=torch.float64)
         rel = torch.empty(6, device=dev, dtype=torch.float64)
         flag = status[slot:] if last else torch.empty(1, device=dev, dtype=torch.int32)
-        _lib.check(lib.sbt_ritz_f64(                     # Q^T Z is formed in-kernel
-            ptr(qz.data_ptr()), None, n, p, rank, float(tol), ptr(ut.data_ptr()),
+        _lib.check(entry(
+            ptr(t.data.data_ptr()), len(dims), cdims, r, ptr(qt.data_ptr()), qt.stride(0), p,
+            rank, float(tol), ptr(ws.data_ptr()), ws.numel(), ptr(ut.data_ptr()),
             ptr(yt.data_ptr() if yt is not None else None),
             ptr(ut32.data_ptr() if ut32 is not None else None), ptr(w.data_ptr()),
-            ptr(flag.data_ptr()), ptr(rel.data_ptr()), stream), "sbt_ritz_f64")
+            ptr(flag.data_ptr()), ptr(rel.data_ptr()), stream), "sbt_hooi_factor")
         if RITZ_LOG is not None:
             RITZ_LOG.append(rel)              # device tensors: diagnostics only
         if not last:
@@ -348,6 +356,22 @@ def _factor_device(t: DenseTensor, r: int, rank: int, warm, status, slot: int,
     if ut32 is not None:
         _attach_f32(u, ut32)       # fp32 copy for the fp32 mode products
     return u
+
+
+def _hooi_status(core: DenseTensor, status, out):
+    """out[0] = ||core||, out[1:] = the factors' flags: one launch
+    (``sbt_hooi_status_*``), the iteration's one device->host read."""
+    import ctypes
+    from . import _lib
+    torch = _torch()
+    lib = _lib.load()
+    ptr = ctypes.c_void_p
+    data = core.data if core.layout.is_packed() else core.view().contiguous().reshape(-1)
+    entry = lib.sbt_hooi_status_f64 if data.dtype == torch.float64 else lib.sbt_hooi_status_f32
+    _lib.check(entry(ptr(data.data_ptr()), data.numel(), ptr(status.data_ptr()), status.numel(),
+                     ptr(out.data_ptr()), ptr(torch.cuda.current_stream(data.device).cuda_stream)),
+               "sbt_hooi_status")
+    return out
 
 
 def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
@@ -540,6 +564,8 @@ class _IterationGraph:
         self.sets32 = [[torch.empty_like(u, dtype=torch.float32) if f32 else None for u in st]
                        for st in self.sets]
         self.status = [torch.zeros(order, dtype=torch.int32, device=t.device) for _ in range(2)]
+        self.out_bufs = [torch.zeros(1 + order, dtype=torch.float64, device=t.device)
+                         for _ in range(2)]
         self.out = [None, None]
         self.graphs = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
         self.cur = 0
@@ -563,15 +589,12 @@ class _IterationGraph:
         return self
 
     def _record(self, k, t, ranks, fast, sweeps):
-        torch = _torch()
-        st = self.status[k]
-        st.zero_()
+        st = self.status[k]                # every flag is written by its Ritz kernel
         nxt = 1 - k
         outs = list(zip(self.sets[nxt], self.sets32[nxt]))
         core = _hooi_sweep(t, self._views(k), fast, lambda y, r, warm: _factor_device(
             y, r, ranks[r], warm, st, r, sweeps, out=outs[r]))
-        norm_g = torch.linalg.vector_norm(core.data.to(torch.float64)).reshape(1)
-        self.out[k] = torch.cat([norm_g, st.to(torch.float64)])
+        self.out[k] = _hooi_status(core, st, self.out_bufs[k])
 
     def replay(self):
         """One iteration from set ``cur`` into the other set; returns the
@@ -637,8 +660,8 @@ def hooi(t: DenseTensor, ranks, max_iters: int = 50, tol: float = 1e-10,
                 status = torch.zeros(order, dtype=torch.int32, device=t.device)
                 core = _hooi_sweep(t, factors, fast, lambda y, r, warm: _factor_device(
                     y, r, ranks[r], warm, status, r, sweeps))
-                norm_g2 = torch.linalg.vector_norm(core.data.to(torch.float64)).reshape(1)
-                vals = torch.cat([norm_g2, status.to(torch.float64)]).cpu().numpy()  # one sync
+                vals = _hooi_status(core, status, torch.empty(
+                    1 + order, dtype=torch.float64, device=t.device)).cpu().numpy()  # one sync
             stats["graph"] = graph is not None
             if np.all(vals[1:] == 1.0):
                 norm_g = float(vals[0])

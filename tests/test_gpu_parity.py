@@ -656,6 +656,77 @@ def test_ritz_kernel_matches_host_rayleigh_ritz(n, rank, fused):
     np.testing.assert_allclose(np.abs(yt.cpu().numpy().T), np.abs(g @ u), atol=1e-8 * hw[0])
 
 
+@pytest.mark.parametrize("dims,mode,rank,dtype", [
+    ((512, 32, 32), 0, 32, "float32"), ((32, 512, 32), 1, 32, "float32"),
+    ((32, 32, 512), 2, 32, "float32"), ((200, 24, 17), 0, 13, "float64"),
+    ((9, 300, 14), 1, 40, "float64"), ((6, 5, 7, 260), 3, 64, "float32"),
+    ((7, 140, 3, 5), 1, 20, "float64")])
+def test_hooi_factor_matches_host_sweep(dims, mode, rank, dtype):
+    """sbt_hooi_factor_* (G Q = Y_(r) (Y_(r)^T Q) straight from the packed
+    tensor, then the Ritz finish) equals the host sweep: Z against the fp64
+    Gram of the mode-r unfolding, the Ritz values / sign-fixed vectors against
+    numpy's Rayleigh-Ritz on the same basis (reference tucker.py:63-76)."""
+    import ctypes
+    from paper_1606_05696_b200 import _lib, tucker as tk
+    rng = np.random.default_rng(sum(dims) + mode)
+    x = rng.standard_normal(dims)
+    x[..., :2] *= 5.0                            # a leading subspace to find
+    t = DenseTensor.from_array(x, dtype=dtype)
+    xr = t.host_data().astype(np.float64).reshape(dims[::-1]).transpose(
+        *reversed(range(len(dims))))             # the tensor's exact (rounded) values
+    n = dims[mode]
+    ymat = np.moveaxis(xr, mode, 0).reshape(n, -1)
+    g = ymat @ ymat.T
+    q = np.linalg.qr(rng.standard_normal((n, rank)))[0]
+    warm = torch.as_tensor(q, device="cuda")
+    status = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    u = tk._factor_device(t, mode, rank, warm, status, 0)
+    torch.cuda.synchronize()
+    # Z = G Q as the library computed it (workspace), fp64 accumulation
+    ws = tk._factor_ws(t.data.device, tuple(dims), mode, rank)
+    cd = (ctypes.c_int64 * len(dims))(*dims)
+    lib = _lib.load()
+    nbytes = lib.sbt_hooi_factor_ws_bytes(len(dims), cd, mode, rank)
+    assert nbytes == ws.numel()
+    z_want = g @ q
+    h = q.T @ z_want
+    hw, hv = np.linalg.eigh(0.5 * (h + h.T))
+    hw, hv = hw[::-1], hv[:, ::-1]
+    uw = q @ hv
+    uw = uw * np.where(uw[np.argmax(np.abs(uw), axis=0), np.arange(rank)] < 0, -1.0, 1.0)
+    np.testing.assert_allclose(u.cpu().numpy(), uw, atol=1e-9)
+    assert status.item() in (0, 1)
+    # the counters are left zero for the next call / replay
+    tail = ws[-4 * ((n + 31) // 32):].cpu().numpy()
+    assert not tail.any()
+
+
+def test_hooi_sharded_device_ops_single_rank_equals_hooi():
+    """parallel.hooi_sharded on the device path (DeviceOps: planned mode
+    products, ring Gram, device-finished factor updates, status kernel) with
+    one NCCL rank gives hooi()'s fits and factors."""
+    import torch.distributed as dist
+    from paper_1606_05696_b200.parallel import hooi_sharded
+    rng = np.random.default_rng(31)
+    dims, ranks = (256, 192, 160), (16, 12, 8)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    dist.init_process_group("nccl", rank=0, world_size=1, store=dist.HashStore(),
+                            device_id=torch.device("cuda", 0))
+    try:
+        for dtype, ftol, utol in (("float64", 1e-12, 1e-9), ("float32", 1e-6, 1e-5)):
+            t = DenseTensor.from_array(full, dtype=dtype)
+            m = sbt.hooi(t, ranks, max_iters=4, tol=-1.0, use_graph=False)
+            _, u, fits, iters = hooi_sharded(t, dims, ranks, max_iters=4, tol=-1.0)
+            assert iters == 4
+            np.testing.assert_allclose(fits, m.fit_history, rtol=0, atol=ftol)
+            for u1, u2 in zip(u, m.factors):
+                np.testing.assert_allclose(u1.cpu().numpy(), u2.cpu().numpy(), atol=utol)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_hooi_device_ritz_equals_host_path():
     """HOOI with the device-finished sweeps (one host sync per iteration)
     gives the host-driven path's fits and factors, fp32 and fp64."""

@@ -88,8 +88,8 @@ int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, 
         dims[mode].  qt: the previous factor's p columns as rows of ldq
         doubles (p <= 64).  Forms Z = Y_(mode) Y_(mode)^T Q in fp64 straight
         from y (no unfolding copy; fp32 widened on load; deterministic) in the
-        caller's workspace `ws` (sbt_hooi_factor_ws_bytes bytes, zero-filled
-        once before its first use; the library leaves it reusable), then
+        caller's workspace `ws` (sbt_hooi_factor_ws_bytes bytes, no
+        initialisation needed), then
         finishes the sweep exactly as sbt_ritz_f64 with m = NULL.  Three
         launches, no host synchronisation, capturable. */
 size_t sbt_hooi_factor_ws_bytes(int order, const int64_t* dims, int mode, int p);
@@ -101,6 +101,16 @@ int sbt_hooi_factor_f64(const double* y, int order, const int64_t* dims, int mod
                         const double* qt, int64_t ldq, int p, int rank, double tol, void* ws,
                         size_t ws_bytes, double* ut, double* yt, float* ut32, double* w,
                         int* flag, double* rel, void* stream);
+/* ---- reference: tucker.py:87-123 (_mode_product_chain), one small product
+        T x_mode U^T with fp64 accumulation: y packed (order, dims), U's p
+        columns as rows of ldq doubles (p <= 64), out packed with extent p at
+        `mode`.  Every output is an fp64 dot product over dims[mode] (fixed
+        order) rounded once: the HOOI core product of fp32 tensors, whose norm
+        the fit compares, carries no tensor-core accumulator truncation. */
+int sbt_mode_product_acc64_f32(const float* y, int order, const int64_t* dims, int mode,
+                               const double* qt, int64_t ldq, int p, float* out, void* stream);
+int sbt_mode_product_acc64_f64(const double* y, int order, const int64_t* dims, int mode,
+                               const double* qt, int64_t ldq, int p, double* out, void* stream);
 /* ---- reference: tucker.py:164-168 (fit from ||G||).  out[0] = ||core||_2
         (fp64 sum of squares over `count` packed elements, fixed order),
         out[1 + f] = flags[f] for f < nflags (<= 64): the HOOI iteration's one

@@ -74,6 +74,10 @@ SIGNATURES = {
                              c_double, _P, ctypes.c_size_t, _P, _P, _P, _P, _P, _P, _P], c_int),
     "sbt_hooi_factor_f64": ([_P, c_int, ctypes.POINTER(c_int64), c_int, _P, c_int64, c_int, c_int,
                              c_double, _P, ctypes.c_size_t, _P, _P, _P, _P, _P, _P, _P], c_int),
+    "sbt_mode_product_acc64_f32": ([_P, c_int, ctypes.POINTER(c_int64), c_int, _P, c_int64, c_int,
+                                    _P, _P], c_int),
+    "sbt_mode_product_acc64_f64": ([_P, c_int, ctypes.POINTER(c_int64), c_int, _P, c_int64, c_int,
+                                    _P, _P], c_int),
     "sbt_hooi_status_f32": ([_P, c_int64, _P, c_int, _P, _P], c_int),
     "sbt_hooi_status_f64": ([_P, c_int64, _P, c_int, _P, _P], c_int),
     "sbt_batched_core_group_f32": ([c_int, ctypes.POINTER(GemmDesc), _P], c_int),

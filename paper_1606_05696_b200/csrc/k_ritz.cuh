@@ -33,7 +33,13 @@ namespace sbt {
 namespace ritz {
 
 #ifdef SBT_RITZ_CLOCK
-__device__ long long g_ritz_clock[2];  // [1]: cycles of the Jacobi steps
+// [0..11]: CTA 0 thread 0 cycles since kernel start at the STAMP points;
+// [15]: cycles of the Jacobi steps
+__device__ long long g_ritz_clock[16];
+#define RITZ_STAMP(k) \
+  do { if (tid == 0 && crank == 0) g_ritz_clock[k] = clock64() - t_start; } while (0)
+#else
+#define RITZ_STAMP(k) do { } while (0)
 #endif
 constexpr int kMaxP = 64;
 constexpr int kHalf = kMaxP / 2;
@@ -149,6 +155,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
       load_tile(i0, rows);
       __syncthreads();
+      RITZ_STAMP(0);
 #pragma unroll
       for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) {
         const int e = tid + t * kThreads;
@@ -167,6 +174,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       const int e = tid + t * kThreads;
       if (e < p * p) Hp[(e / p) * LDS + e % p] = hacc[t];
     }
+    RITZ_STAMP(1);
     cluster.sync();
     // each CTA sums a slice of the entries over the cluster (CTA order, the
     // eight remote loads in flight together) into CTA 0's slot 3
@@ -183,6 +191,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       H0[off] = sum;
     }
     cluster.sync();
+    RITZ_STAMP(2);
   }
   if (crank == 0) {  // the eigen phase runs on CTA 0; the others wait
     // round-robin schedule (circle method: position 0 holds player P-1) and
@@ -232,6 +241,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
     // sqrt(a_pp a_qq) would keep rotating rounding noise between the smallest
     // Ritz values)
     const double floor_abs = fmax(1e-15, 1e-2 * tol) * sqrt(s_red[0]);
+    RITZ_STAMP(3);
     // rotation of pair (a, b) from the current A: J[a][a] = J[b][b] = c,
     // J[a][b] = s, J[b][a] = -s.  t = tan(angle) at float precision (any t
     // gives an orthogonal rotation; |th| <= 2e15 above the floor), c = (1 +
@@ -310,6 +320,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       }
       __syncthreads();
     }
+    RITZ_STAMP(4);
     int cur = 0;
     for (int sweep = 0; sweep < 40; ++sweep) {
       // converged when no off-diagonal element exceeds the floor
@@ -380,12 +391,13 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
         cur ^= 1;
         __syncthreads();
   #ifdef SBT_RITZ_CLOCK
-        if (tid == 0) g_ritz_clock[1] += clock64() - c0;
+        if (tid == 0) g_ritz_clock[15] += clock64() - c0;
   #endif
       }
     }
     const double* A = smr + cur * MAT;
     t_jacobi = clock64();
+    RITZ_STAMP(5);
 
     // descending order of the p true eigenvalues (the padding index is excluded)
     if (tid < p) {
@@ -412,8 +424,10 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       w[tid] = wv[tid];
     }
   }
+  RITZ_STAMP(6);
   // ---- Ritz vectors, residuals and sign rule on all CTAs of the cluster ----
   cluster.sync();
+  RITZ_STAMP(7);
   if (crank != 0) {  // copy the sorted eigenvectors / values from CTA 0
     const double* rVs = cluster.map_shared_rank(Vs, 0);
     const double* rwv = cluster.map_shared_rank(wv, 0);
@@ -507,9 +521,11 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       if ((tid & 31) == 0 && mx[jj] == amax[j]) atomicMin(&s_arg[j], ax[jj]);
     }
   }
+  RITZ_STAMP(8);
   __threadfence();  // U entries (global) visible to the cluster after the barrier
   cluster.sync();
   const long long t_ritz = clock64();
+  RITZ_STAMP(9);
   // sign rule (tucker.py:71-75): combine the CTAs' (max, first index) per
   // column, then every CTA negates its own rows of negative columns
   if (tid < rank) {
@@ -554,7 +570,9 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
       rel[5] = double(newton);
     }
   }
+  RITZ_STAMP(10);
   cluster.sync();  // no CTA exits while its shared memory may still be read
+  RITZ_STAMP(11);
 }
 
 }  // namespace ritz

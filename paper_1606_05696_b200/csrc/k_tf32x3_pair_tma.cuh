@@ -231,7 +231,7 @@ struct FlushCfg {
   static constexpr int ACC_W = (SPLIT_ACC ? 2 : 1) * BNT;
   static constexpr int NBUF = 512 / ACC_W >= 2 ? 2 : 1;
   static constexpr int BASE = NBUF * ACC_W;
-  static constexpr int NSLOT = ON ? ((512 - BASE) / BNT < 8 ? (512 - BASE) / BNT : 8) : 1;
+  static constexpr int NSLOT = ON ? ((512 - BASE) / BNT < 12 ? (512 - BASE) / BNT : 12) : 1;
 };
 
 template <int MAXP, bool SPLIT_ACC, int BK, bool BB = false, int BNT = 256, int EPIB = 2>
@@ -270,7 +270,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
   uint64_t* step_empty = step_full + NSLOT;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(step_empty + NSLOT);
   static_assert((3 * RAW_SLOTS + LO_SLOTS + 4 + 2 * NSLOT) * 8 + 4 <= 512, "barrier area");
-  // FLUSH: K=8 steps per step-accumulator group (1, 2 or 4; log2 in bits 12-13)
+  // FLUSH: K=8 steps per step-accumulator group (1, 2, 4 or 8; log2 in bits 12-13)
   const int flush_lg = (p_prefetch >> 12) & 3;
 
   const int tid = threadIdx.x;
@@ -516,7 +516,8 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
       if constexpr (FLUSH) {
 #pragma unroll
         for (int j = 0; j < BNT; ++j) facc[j] = 0.f;
-        const uint32_t ngroups = uint32_t(P.nkb * (BK / 8)) >> flush_lg;
+        const int lg_t = (flush_lg == 3 && (P.nkb & 1)) ? 2 : flush_lg;
+        const uint32_t ngroups = uint32_t(P.nkb * (BK / 8)) >> lg_t;
 #pragma unroll 1
         for (uint32_t gi = 0; gi < ngroups; ++gi, ++eg) {
           const uint32_t slot = eg % NSLOT;
@@ -787,7 +788,7 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
     // SBO 512 (4-row K groups), K=8 step = 1024 B.
     constexpr uint32_t k_lay = BK == 32 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
     uint32_t it = 0, tcount = 0;
-    uint32_t u = 0;  // FLUSH: K=8 steps issued (all tiles)
+    uint32_t u = 0, u_in = 0;  // FLUSH: step groups started (all tiles), steps in the current one
     int cur = 0;
     for (int64_t t = pair; t < total; t += npairs, ++tcount) {
       const Problem& P = prob(t, cur);
@@ -820,10 +821,12 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
         // BB: A_hi is the converter's swizzled copy, not the dense raw box
         const uint32_t a_raw = BB ? a_lo + Gm::SLOT_BYTES : b_raw - Gm::A_BYTES;
         if constexpr (FLUSH) {
-          const uint32_t gmask = (1u << flush_lg) - 1u;
+          // group size 2^lg_t K=8 steps; 8-step groups need an even K-block count
+          const int lg_t = (flush_lg == 3 && (nkb & 1)) ? 2 : flush_lg;
+          const uint32_t gmask = (1u << lg_t) - 1u;
 #pragma unroll
-          for (int j = 0; j < BK / 8; ++j, ++u) {
-            const uint32_t grp = u >> flush_lg, slot = grp % NSLOT, within = u & gmask;
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t grp = u, slot = grp % NSLOT, within = u_in;
             if (within == 0) {  // the epilogue drained this slot's previous group
               ptx::mbar_wait(&step_empty[slot], ((grp / NSLOT) & 1u) ^ 1u);
               ptx::tc_fence_after();
@@ -843,6 +846,8 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
               }
             }
             __syncwarp();
+            if (within == gmask) ++u, u_in = 0;
+            else ++u_in;
           }
         } else if (ptx::elect_one_sync()) {
 #pragma unroll

@@ -558,7 +558,7 @@ namespace {
 // the unfolding geometry of a packed tensor (k_gram_apply.cuh)
 int unfold_of(int order, const int64_t* dims, int mode, sbt::gapply::Unfold& u) {
   if (order < 1 || order > 16 || !dims || mode < 0 || mode >= order) return -1;
-  int64_t a = 1, total = 1;
+  int64_t a = 1, total = 1;  // (the kernels keep A = prod(d_<mode) in 32 bits)
   for (int i = 0; i < order; ++i) {
     if (dims[i] < 1) return -1;
     if (i < mode) a *= dims[i];
@@ -567,7 +567,28 @@ int unfold_of(int order, const int64_t* dims, int mode, sbt::gapply::Unfold& u) 
   u.n = dims[mode];
   u.cols = total / u.n;
   u.A = a;
-  return 0;
+  return a < (int64_t(1) << 31) ? 0 : -1;
+}
+
+template <typename TY, typename TO, bool MODE_OUT>
+int launch_w(const TY* y, const sbt::gapply::Unfold& u, const double* qt, int64_t ldq, int p,
+             TO* out, cudaStream_t stream) {
+  using namespace sbt;
+  const int ys = int(sizeof(TY));
+  const int rch = gapply::w_rows_per_chunk(u.n, p, ys);
+  const int smem = int(gapply::w_smem_bytes(rch, p, ys));
+  auto kern = gapply::w_kernel<TY, TO, MODE_OUT>;
+  // the attribute is set once per (kernel, device): the largest chunk any call uses
+  int rc = set_smem_attr(reinterpret_cast<const void*>(kern), gapply::W_SMEM_MAX + 1024);
+  if (rc != SBT_OK) return rc;
+  // 1-D bulk copies need 16-byte aligned rows of a multiple of 16 bytes
+  const bool qbulk = reinterpret_cast<uintptr_t>(qt) % 16 == 0 && ldq % 2 == 0 && u.n % 2 == 0;
+  const bool ybulk = u.A == 1 && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+                     (u.n * ys) % 16 == 0;
+  kern<<<unsigned(ceil_div(u.cols, gapply::CB)), gapply::NT, smem, stream>>>(
+      y, u, qt, ldq, p, out, rch, (qbulk ? 1 : 0) | (ybulk ? 2 : 0));
+  note_launch(MODE_OUT ? "mode_product_acc64" : "gram_apply_w");
+  return check_cuda(cudaGetLastError(), "gram_apply w_kernel launch");
 }
 
 template <typename TY>
@@ -586,19 +607,18 @@ int hooi_factor(const TY* y, int order, const int64_t* dims, int mode, const dou
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   double* wsd = static_cast<double*>(ws);
   double* wt = wsd + pl.w_off;
-  double* part = wsd + pl.part_off;
   double* zt = wsd + pl.z_off;
-  unsigned* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + pl.cnt_off_bytes);
-  gapply::w_kernel<TY><<<unsigned(ceil_div(u.cols, gapply::CB)), gapply::NT, 0, stream>>>(
-      y, u, qt, ldq, p, wt);
-  note_launch("gram_apply_w");
-  int rc = check_cuda(cudaGetLastError(), "gram_apply_w launch");
+  // diagnostics (tools/factor_bench.py): 1 = W only, 2 = W and Z, else all
+  static const int stop_after = env_int("SBT_GA_DEBUG", 0);
+  int rc = launch_w<TY, double, false>(y, u, qt, ldq, p, wt, stream);
+  if (rc != SBT_OK || stop_after == 1) return rc;
+  rc = set_smem_attr(reinterpret_cast<const void*>(gapply::z_kernel<TY>), gapply::Z_SMEM_BYTES);
   if (rc != SBT_OK) return rc;
-  gapply::z_kernel<TY><<<dim3(unsigned(pl.tiles), unsigned(pl.splits)), gapply::NT, 0, stream>>>(
-      y, u, wt, p, pl.kper, zt, u.n, part, cnt);
+  gapply::z_kernel<TY><<<dim3(unsigned(pl.tiles), unsigned(gapply::ZS)), gapply::NT,
+                         gapply::Z_SMEM_BYTES, stream>>>(y, u, wt, p, pl.kper, zt, u.n);
   note_launch("gram_apply_z");
   rc = check_cuda(cudaGetLastError(), "gram_apply_z launch");
-  if (rc != SBT_OK) return rc;
+  if (rc != SBT_OK || stop_after == 2) return rc;
   rc = set_smem_attr(reinterpret_cast<const void*>(ritz::ritz_kernel), ritz::SMEM_BYTES);
   if (rc != SBT_OK) return rc;
   ritz::ritz_kernel<<<ritz::kCluster, ritz::kThreads, ritz::SMEM_BYTES, stream>>>(
@@ -619,9 +639,45 @@ int hooi_status(const T* x, int64_t count, const int* flags, int nflags, double*
   return check_cuda(cudaGetLastError(), "hooi_status launch");
 }
 
+template <typename T>
+int mode_product_acc64(const T* y, int order, const int64_t* dims, int mode, const double* qt,
+                       int64_t ldq, int p, T* out, void* stream) {
+  using namespace sbt;
+  gapply::Unfold u;
+  if (!y || !qt || !out || unfold_of(order, dims, mode, u) || p < 1 || p > gapply::kMaxP ||
+      ldq < u.n)
+    return fail(SBT_EINVAL, "sbt_mode_product_acc64: bad arguments");
+  return launch_w<T, T, true>(y, u, qt, ldq, p, out, static_cast<cudaStream_t>(stream));
+}
+
 }  // namespace
 
 extern "C" {
+
+#ifdef SBT_RITZ_CLOCK
+// diagnostics build only (tools/ritz_probe.py with SBT_LIB): the Ritz
+// kernel's phase stamps of the last launch
+int sbt_ritz_clock(long long* out) {
+  return cudaMemcpyFromSymbol(out, sbt::ritz::g_ritz_clock, 16 * sizeof(long long)) ==
+                 cudaSuccess ? 0 : -3;
+}
+int sbt_ga_clock(long long* out) {
+  return (cudaMemcpyFromSymbol(out, sbt::gapply::g_ga_clock, 8 * sizeof(long long)) ==
+              cudaSuccess &&
+          cudaMemcpyFromSymbol(out + 8, sbt::gapply::g_gz_clock, 8 * sizeof(long long)) ==
+              cudaSuccess) ? 0 : -3;
+}
+#endif
+
+int sbt_mode_product_acc64_f32(const float* y, int order, const int64_t* dims, int mode,
+                               const double* qt, int64_t ldq, int p, float* out, void* stream) {
+  return mode_product_acc64<float>(y, order, dims, mode, qt, ldq, p, out, stream);
+}
+
+int sbt_mode_product_acc64_f64(const double* y, int order, const int64_t* dims, int mode,
+                               const double* qt, int64_t ldq, int p, double* out, void* stream) {
+  return mode_product_acc64<double>(y, order, dims, mode, qt, ldq, p, out, stream);
+}
 
 size_t sbt_hooi_factor_ws_bytes(int order, const int64_t* dims, int mode, int p) {
   sbt::gapply::Unfold u;

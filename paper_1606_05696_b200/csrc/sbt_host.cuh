@@ -30,8 +30,11 @@ namespace host {
 class CopyPool {
  public:
   static CopyPool& get() {
-    static CopyPool pool;
-    return pool;
+    // never destroyed: the detached workers wait on cv_ for the life of the
+    // process, and destroying a condition variable with waiters at exit
+    // blocks (glibc) -- the process would hang in its static destructors
+    static CopyPool* pool = new CopyPool;
+    return *pool;
   }
   // memcpy split into `parts` pieces run on the workers (and this thread)
   void copy(void* dst, const void* src, size_t bytes) {

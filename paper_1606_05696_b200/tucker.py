@@ -283,9 +283,8 @@ _FACTOR_WS = {}
 
 
 def _factor_ws(dev, dims, r, p):
-    """Workspace of sbt_hooi_factor for (dims, mode, p): allocated zero-filled
-    once per device and reused (the library leaves it reusable), so a captured
-    iteration allocates nothing."""
+    """Workspace of sbt_hooi_factor for (dims, mode, p): allocated once per
+    device and reused, so a captured iteration allocates nothing."""
     import ctypes
     from . import _lib
     torch = _torch()
@@ -374,9 +373,47 @@ def _hooi_status(core: DenseTensor, status, out):
     return out
 
 
+# small fp32 products T x_r U^T (at most this many input elements; the HOOI
+# core product y2 x_2 U_2^T at 512^3 rank 32 reads 2^19) run with fp64
+# accumulation (sbt_mode_product_acc64_f32): the fit compares ||G|| with ||T||
+# and amplifies a relative error of ||G|| ~15x (resid / ||T|| ~ 0.064), so the
+# core must not carry the tensor core's accumulator truncation (~2e-6 at
+# K = 512 on a 128-row tile).  The large products run on the unbiased
+# narrow-tile (FLUSH) path of the CTA-pair kernel.
+_ACC64_MAX_ELEMS = 1 << 21
+
+
+def _mode_product_acc64(cur: DenseTensor, u, r: int) -> DenseTensor:
+    import ctypes
+    from . import _lib
+    torch = _torch()
+    dims = tuple(int(d) for d in cur.layout.dims)
+    rank = int(u.shape[1])
+    qt = torch.as_tensor(u, device=cur.data.device, dtype=torch.float64).t()
+    if qt.stride(1) != 1:
+        qt = qt.contiguous()
+    out_dims = list(dims)
+    out_dims[r] = rank
+    out = DenseTensor.empty(Layout.packed(out_dims), dtype=cur.dtype, device=cur.device)
+    lib = _lib.load()
+    fn = lib.sbt_mode_product_acc64_f32 if cur.dtype == torch.float32 else \
+        lib.sbt_mode_product_acc64_f64
+    ptr = ctypes.c_void_p
+    _lib.check(fn(ptr(cur.data.data_ptr()), len(dims), (ctypes.c_int64 * len(dims))(*dims), r,
+                  ptr(qt.data_ptr()), qt.stride(0), rank, ptr(out.data.data_ptr()),
+                  ptr(torch.cuda.current_stream(cur.data.device).cuda_stream)),
+               "sbt_mode_product_acc64")
+    return out
+
+
 def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
     """One planned contraction T x_r U^T (transpose) or T x_r U."""
     order = cur.layout.order
+    torch = _torch()
+    if (transpose and cur.dtype == torch.float32 and cur.layout.is_packed()
+            and cur.layout.size <= _ACC64_MAX_ELEMS and u.shape[1] <= 64
+            and getattr(u, "is_cuda", False)):
+        return _mode_product_acc64(cur, u, r)
     rows, cols = u.shape
     labels_b, out_ext = (("k", "z"), cols) if transpose else (("z", "k"), rows)
     labels_a = tuple("k" if i == r else _LETTERS[i] for i in range(order))

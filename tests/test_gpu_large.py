@@ -177,4 +177,5 @@ def test_hooi_c4_fp32_matches_fp64_oracle():
         u = model.factors[k].cpu().numpy()
         ur = ref["factors"][k]
         np.testing.assert_allclose(u @ u.T, ur @ ur.T, atol=1e-5)
-    sbt.clear_graph_cache()
+    from paper_1606_05696_b200 import tucker as tk
+    tk.clear_graph_cache()

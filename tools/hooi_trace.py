@@ -46,3 +46,16 @@ for m in (1, 5):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     sbt.hooi(t, (r, r, r), max_iters=m, tol=-1.0); torch.cuda.synchronize()
     print("wall hooi", m, (time.perf_counter() - t0) * 1e3)
+
+# per-launch durations of one iteration (the last 5-iteration run's final iteration)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    sbt.hooi(t, (r, r, r), max_iters=3, tol=-1.0)
+    torch.cuda.synchronize()
+evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+evs.sort(key=lambda e: e.time_range.start)
+tail = evs[-40:]
+print("last launches (us):")
+for e in tail:
+    d = e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+    print(f"  {d:8.1f}  {e.name[:90]}")

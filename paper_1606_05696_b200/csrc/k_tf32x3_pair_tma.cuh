@@ -140,6 +140,7 @@ __device__ long long g_trace[8][4096];
 __device__ long long g_trace_epi[2][64][4];
 __device__ long long g_trace_mma[64][2];       // per tile: accumulator acquired, last commit
 __device__ long long g_trace_tepi[2][64][8];   // TMA-store epilogue: wait, acquired, released, end, phase sums
+__device__ long long g_trace_flush[2][4096];   // FLUSH: epilogue warp 0 got step group eg
 #else
 #define TRACE(row, idx) do { } while (0)
 #endif
@@ -523,6 +524,9 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
           const uint32_t slot = eg % NSLOT;
           ptx::mbar_wait(&step_full[slot], (eg / NSLOT) & 1u);
           ptx::tc_fence_after();
+#ifdef SBT_TRACE
+          if (blockIdx.x < 2 && tid == 0 && eg < 4096) g_trace_flush[rank][eg] = clock64();
+#endif
           uint32_t v[BNT];
 #pragma unroll
           for (int c = 0; c < BNT; c += 16)
@@ -821,32 +825,43 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
         // BB: A_hi is the converter's swizzled copy, not the dense raw box
         const uint32_t a_raw = BB ? a_lo + Gm::SLOT_BYTES : b_raw - Gm::A_BYTES;
         if constexpr (FLUSH) {
-          // group size 2^lg_t K=8 steps; 8-step groups need an even K-block count
+          // group size 2^lg_t K=8 steps; 8-step groups need an even K-block count.
+          // One elected lane issues the whole K-block (and waits for the step
+          // slots it opens), as in the default path: per-step warp-wide elect /
+          // syncwarp rounds doubled the K-block issue time.
           const int lg_t = (flush_lg == 3 && (nkb & 1)) ? 2 : flush_lg;
           const uint32_t gmask = (1u << lg_t) - 1u;
+          if (ptx::elect_one_sync()) {
+            uint32_t gu = u, gin = u_in;
 #pragma unroll
-          for (int j = 0; j < BK / 8; ++j) {
-            const uint32_t grp = u, slot = grp % NSLOT, within = u_in;
-            if (within == 0) {  // the epilogue drained this slot's previous group
-              ptx::mbar_wait(&step_empty[slot], ((grp / NSLOT) & 1u) ^ 1u);
-              ptx::tc_fence_after();
-            }
-            if (ptx::elect_one_sync()) {
+            for (int j = 0; j < BK / 8; ++j) {
+              const uint32_t slot = gu % NSLOT;
+              if (gin == 0) {  // the epilogue drained this slot's previous group
+                ptx::mbar_wait(&step_empty[slot], ((gu / NSLOT) & 1u) ^ 1u);
+                ptx::tc_fence_after();
+              }
               const uint64_t dar = ptx::umma_desc(a_raw + j * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t dal = ptx::umma_desc(a_lo + j * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t dbr = ptx::umma_desc(b_raw + j * b_step, b_lbo, b_sbo, b_lay);
               const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
               ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, (kb | j) ? 1u : 0u);
               ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
-              ptx::mma2_tf32_ss(tmem + FC::BASE + slot * BNT, dar, dbr, idesc, within ? 1u : 0u);
-              if (within == gmask) ptx::tc_commit2_mc(&step_full[slot], 0x3);
-              if (j == BK / 8 - 1) {
-                ptx::tc_commit2_mc(&raw_empty[s], 0x3);
-                ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
+              ptx::mma2_tf32_ss(tmem + FC::BASE + slot * BNT, dar, dbr, idesc, gin ? 1u : 0u);
+              if (gin == gmask) {
+                ptx::tc_commit2_mc(&step_full[slot], 0x3);
+                ++gu;
+                gin = 0;
+              } else {
+                ++gin;
               }
             }
-            __syncwarp();
-            if (within == gmask) ++u, u_in = 0;
+            ptx::tc_commit2_mc(&raw_empty[s], 0x3);
+            ptx::tc_commit2_mc(&lo_empty[ls], 0x3);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {   // the same step accounting on every lane
+            if (u_in == gmask) ++u, u_in = 0;
             else ++u_in;
           }
         } else if (ptx::elect_one_sync()) {

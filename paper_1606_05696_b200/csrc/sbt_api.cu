@@ -654,6 +654,20 @@ int mode_product_acc64(const T* y, int order, const int64_t* dims, int mode, con
 
 extern "C" {
 
+#ifdef SBT_TRACE
+// diagnostics build only (tools/flush_trace.py): the CTA-pair kernel's timeline
+// of the last launch (pair 0): which 0 = g_trace [8][4096], 1 = g_trace_flush
+// [2][4096], 2 = g_trace_epi [2][64][4], 3 = g_trace_mma [64][2]
+int sbt_trace_dump(int which, long long* out) {
+  cudaError_t e = cudaErrorInvalidValue;
+  if (which == 0) e = cudaMemcpyFromSymbol(out, sbt::tf32tma::g_trace, sizeof(sbt::tf32tma::g_trace));
+  if (which == 1) e = cudaMemcpyFromSymbol(out, sbt::tf32tma::g_trace_flush, sizeof(sbt::tf32tma::g_trace_flush));
+  if (which == 2) e = cudaMemcpyFromSymbol(out, sbt::tf32tma::g_trace_epi, sizeof(sbt::tf32tma::g_trace_epi));
+  if (which == 3) e = cudaMemcpyFromSymbol(out, sbt::tf32tma::g_trace_mma, sizeof(sbt::tf32tma::g_trace_mma));
+  return e == cudaSuccess ? 0 : -3;
+}
+#endif
+
 #ifdef SBT_RITZ_CLOCK
 // diagnostics build only (tools/ritz_probe.py with SBT_LIB): the Ritz
 // kernel's phase stamps of the last launch

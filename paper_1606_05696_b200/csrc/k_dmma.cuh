@@ -19,13 +19,17 @@
 namespace sbt {
 namespace dmma {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+#ifndef SBT_DMMA_BK
+#define SBT_DMMA_BK 16
+#endif
+constexpr int BM = 128, BN = 128, BK = SBT_DMMA_BK, STAGES = 3;
+static_assert(BK == 16 || BK == 32, "K-block depth");
 constexpr int kThreads = 256;      // staging loops assume >= 256 threads
 template <int NW>
 struct WarpGrid {                    // NW = 8: 2 x 4 warps of 64 x 32; 16: 4 x 4 of 32 x 32
   static constexpr int WM = NW / 4, TM = 128 / WM / 8;  // warp rows, DMMA tiles per warp row
 };
-constexpr int LDK = 20;   // [mn][k] rows (16 k + 4 pad)
+constexpr int LDK = BK + 4;   // [mn][k] rows (BK k + 4 pad: rows 8 words apart in the banks)
 constexpr int LDMN = 132; // [k][mn] rows (128 mn + 4 pad)
 // Batch-blocked A (the exceptional cases: A unit-stride along the batch, B
 // batch-independent): the tile's 128 MMA rows are 4 batch entries x 32 m,
@@ -36,8 +40,8 @@ constexpr int LDMN = 132; // [k][mn] rows (128 mn + 4 pad)
 // loads.  A fragment (8 consecutive R) is 8 consecutive m of one batch entry,
 // so the epilogue stores 64-byte runs of C exactly as for plain tiles.
 constexpr int LDBB = 148;
-constexpr int TILE_DOUBLES = 128 * LDK > 16 * LDMN ? 128 * LDK : 16 * LDMN;  // 2560 vs 2112
-static_assert(16 * LDBB <= TILE_DOUBLES, "BB tile fits the stage");
+constexpr int TILE_RAW = 128 * LDK > BK * LDMN ? 128 * LDK : BK * LDMN;  // BK 16: 2560 vs 2112
+constexpr int TILE_DOUBLES = TILE_RAW > BK * LDBB ? TILE_RAW : BK * LDBB;
 constexpr int SMEM_BYTES = STAGES * 2 * TILE_DOUBLES * 8;                   // 120 KB
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
@@ -72,10 +76,10 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
                                               int64_t mn0, int64_t k0, int64_t mn_ext,
                                               int64_t k_ext, int64_t s_mn, int64_t s_k, int tid) {
 #pragma unroll
-  for (int i = 0; i < 1024 / NT; ++i) {  // 1024 chunks of 2 doubles
+  for (int i = 0; i < 64 * BK / NT; ++i) {  // 128 x BK doubles in 16-byte chunks
     const int e = tid + i * NT;
     if (KMAJ) {
-      const int mn = e >> 3, k2 = (e & 7) * 2;
+      const int mn = e / (BK / 2), k2 = (e % (BK / 2)) * 2;
       const int64_t gm = mn0 + mn, gk = k0 + k2;
       const bool ok = gm < mn_ext && gk < k_ext;
       cp_async16(dst + mn * LDK + k2, ok ? src + gm * s_mn + gk : src, ok);
@@ -88,13 +92,13 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
   }
 }
 
-// BB A staging: 128 rows (4 batch x 32 m) x 16 k, 8-byte chunks
+// BB A staging: 128 rows (4 batch x 32 m) x BK k, 8-byte chunks
 template <int NT = kThreads>
 __device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__ src, int64_t b0,
                                          int64_t m0, int64_t k0, int64_t nbatch, int64_t m_ext,
                                          int64_t k_ext, int64_t ars, int64_t acs, int tid) {
 #pragma unroll
-  for (int i = 0; i < 2048 / NT; ++i) {
+  for (int i = 0; i < 128 * BK / NT; ++i) {
     const int e = tid + i * NT;
     const int k = e >> 7, b = e & 3, m = (e >> 2) & 31;
     const int64_t gb = b0 + b, gm = m0 + m, gk = k0 + k;

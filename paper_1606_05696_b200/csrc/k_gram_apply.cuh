@@ -40,7 +40,14 @@ struct Unfold {
 };
 
 // element offset of column c of the unfolding (row 0); row i adds i * A
+// (32-bit division when the column index fits: 64-bit division is a long
+// software sequence)
 __device__ __forceinline__ int64_t col_base(const Unfold& u, int64_t c) {
+  if (c < (int64_t(1) << 31)) {
+    const uint32_t a = uint32_t(u.A), cc = uint32_t(c);
+    const uint32_t q = cc / a;
+    return int64_t(cc - q * a) + int64_t(q) * u.A * u.n;
+  }
   return (c % u.A) + (c / u.A) * u.A * u.n;
 }
 
@@ -345,8 +352,17 @@ z_kernel(const TY* __restrict__ y, Unfold u, const double* __restrict__ wt, int 
       const int mt = ot % (RB / 8), nt = ot / (RB / 8);
       const double* ya = Ys + (8 * mt + fr) * LDY + fk;
       const double* wb = Ws + fk * LDW + 8 * nt + fr;
-#pragma unroll 4
-      for (int k = 0; k < kn4; k += 4) dmma8x8x4(acc[q], ya[k], wb[k * LDW]);
+      double a4[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // k-step chains
+      int k = 0;
+      for (; k + 12 < kn4; k += 16) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma8x8x4(a4[c], ya[k + 4 * c], wb[(k + 4 * c) * LDW]);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)          // tail: at most 3 steps
+        if (k + 4 * c < kn4) dmma8x8x4(a4[c], ya[k + 4 * c], wb[(k + 4 * c) * LDW]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[q][h] += (a4[0][h] + a4[1][h]) + (a4[2][h] + a4[3][h]);
     }
     __syncthreads();
   }
@@ -365,15 +381,19 @@ z_kernel(const TY* __restrict__ y, Unfold u, const double* __restrict__ wt, int 
   GZ_STAMP(4);
   const int crank = int(cluster.block_rank());
   const int nout = nrows * p, per = (nout + ZS - 1) / ZS;
-  for (int e = crank * per + tid; e < (crank + 1) * per && e < nout; e += NT) {
-    const int row = e % nrows, j = e / nrows;    // stores coalesced along i
-    double v[ZS];
-#pragma unroll
-    for (int c = 0; c < ZS; ++c) v[c] = *cluster.map_shared_rank(part + row * kMaxP + j, c);
-    double sum = 0.0;
-#pragma unroll
-    for (int c = 0; c < ZS; ++c) sum += v[c];
-    zt[int64_t(j) * ldz + r0 + row] = sum;
+  // 4 threads per output (2 splits each), pairs then quads summed by shuffles:
+  // ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)), a fixed order
+  static_assert(ZS == 8, "4 lanes x 2 splits");
+  const int sub = tid & 3;
+  for (int e0 = crank * per; e0 < (crank + 1) * per && e0 < nout; e0 += NT / 4) {
+    const int e = e0 + (tid >> 2);
+    const bool ok = e < (crank + 1) * per && e < nout;
+    const int row = ok ? e % nrows : 0, j = ok ? e / nrows : 0;   // stores coalesced along i
+    const double* a = part + row * kMaxP + j;
+    double v = *cluster.map_shared_rank(a, 2 * sub) + *cluster.map_shared_rank(a, 2 * sub + 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (ok && sub == 0) zt[int64_t(j) * ldz + r0 + row] = v;
   }
   GZ_STAMP(5);
   cluster.sync();   // no CTA exits while its partial may still be read

@@ -35,7 +35,7 @@ namespace ritz {
 #ifdef SBT_RITZ_CLOCK
 // [0..11]: CTA 0 thread 0 cycles since kernel start at the STAMP points;
 // [15]: cycles of the Jacobi steps
-__device__ long long g_ritz_clock[16];
+__device__ long long g_ritz_clock[24];
 #define RITZ_STAMP(k) \
   do { if (tid == 0 && crank == 0) g_ritz_clock[k] = clock64() - t_start; } while (0)
 #else
@@ -45,12 +45,12 @@ constexpr int kMaxP = 64;
 constexpr int kHalf = kMaxP / 2;
 constexpr int kThreads = 512;
 constexpr int kCluster = 8;                    // CTAs sharing the Ritz-vector phase
-constexpr int LDS = kMaxP + 1;
+constexpr int LDS = kMaxP + 4;                 // 8-word row skew: conflict-free DMMA row fragments
 constexpr int MAT = kMaxP * LDS;               // one P x P matrix (padded rows)
 constexpr int kTileRows = 64;                  // Q / Z row tile
-constexpr int LDT = kTileRows + 1;             // tile row stride (conflict-free column walks)
+constexpr int LDT = kTileRows + 4;             // tile row stride (conflict-free DMMA fragments)
 constexpr int REGION0 = 5 * MAT;  // >= the two Q / Z tiles (2 * kMaxP * LDT)
-static_assert(2 * kMaxP * LDT <= 4 * MAT, "Q / Z tiles must leave slot 4 free");
+static_assert(2 * kMaxP * LDT <= 2 * MAT, "Q / Z tiles fill slots 0-1; U / Y tiles use 2-3");
 constexpr int kTri = kHalf * (kHalf + 1) / 2;  // upper-triangular 2 x 2 blocks
 constexpr int SMEM_BYTES =
     (REGION0 + 4 * kMaxP) * 8 + (2 * kMaxP) * 4 + (kMaxP * kMaxP + 2 * kTri) + 64;
@@ -58,7 +58,7 @@ constexpr int SMEM_BYTES =
 // C = op(X) Y for P x P matrices in shared memory (row stride LDS), 2 x 2
 // register blocks per thread; EPI 1 stores 1.5 I - 0.5 C (Newton-Schulz).
 template <bool TX, int EPI>
-__device__ __forceinline__ void small_mm(const double* X, const double* Y, double* C, int P,
+__device__ __forceinline__ void small_mm_unused(const double* X, const double* Y, double* C, int P,
                                          int tid) {
   const int hb = P / 2;
   for (int blk = tid; blk < hb * hb; blk += kThreads) {
@@ -83,6 +83,56 @@ __device__ __forceinline__ void small_mm(const double* X, const double* Y, doubl
     C[i0 * LDS + j0 + 1] = c01;
     C[(i0 + 1) * LDS + j0] = c10;
     C[(i0 + 1) * LDS + j0 + 1] = c11;
+  }
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// C = op(X) Y for P x P matrices in shared memory (row stride LDS) on the
+// fp64 tensor pipe: 8 x 8 DMMA output tiles over the 16 warps, two
+// accumulator chains per tile (even / odd k-steps, summed at the end: a fixed
+// order); k >= P reads as zero, rows / columns >= P are not stored.  EPI 1
+// stores 1.5 I - 0.5 C (Newton-Schulz).  All threads of the CTA call it.
+// One out-of-line copy (runtime TX / EPI): the serial eigen phase runs each
+// code path a few times only, so instruction-cache misses on cold inlined
+// copies cost more than the arithmetic.
+__device__ __noinline__ void dmma_mm_rt(const double* X, const double* Y, double* C, int P,
+                                        int tid, bool TX, int EPI) {
+  const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+  const int nt = (P + 7) >> 3;
+  for (int t = warp; t < nt * nt; t += kThreads / 32) {
+    const int mt = t / nt, ntl = t % nt;
+    const int m = 8 * mt + fr, n = 8 * ntl + fr;
+    // k-step s accumulates into chain s % 8: the fp64 tensor pipe's long
+    // dependent-issue latency would otherwise serialise the P / 4 steps
+    double c[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+    for (int k0 = 0; k0 < P; k0 += 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = k0 + 4 * q + fk;
+        const double a = k < P ? (TX ? X[k * LDS + m] : X[m * LDS + k]) : 0.0;
+        const double b = k < P ? Y[k * LDS + n] : 0.0;
+        dmma(c[q], a, b);
+      }
+    }
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c0[0] += c[q][0], c0[1] += c[q][1];
+    const int row = 8 * mt + fr;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = 8 * ntl + 2 * fk + h;
+      if (row < P && col < P) {
+        const double v = c0[h] + c1[h];
+        C[row * LDS + col] = EPI == 1 ? (row == col ? 1.5 : 0.0) - 0.5 * v : v;
+      }
+    }
   }
 }
 
@@ -111,6 +161,8 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
   double* W = smr + MAT;
   double* Qs = smr;                     // [p][LDT] row tiles (reuse A / V)
   double* Zs = smr + kMaxP * LDT;
+  double* Us = smr + 2 * MAT;           // Ritz phase: U / Y row tiles [64][LDS]
+  double* Yv = smr + 3 * MAT;
   double* Vs = smr + 4 * MAT;           // [p][LDS]: sorted leading eigenvectors (reuses S)
   double* wv = smr + REGION0;           // sorted eigenvalues
   double* res = wv + kMaxP;             // [rank] squared residuals
@@ -148,31 +200,44 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
   // slot 4, summed in CTA order by CTA 0) instead of a separate GEMM
   double* Hp = smr + 4 * MAT;
   if (m == nullptr) {
-    double hacc[kMaxP * kMaxP / kThreads];
+    // partial H = Q_t^T Z_t over this CTA's row tiles on the fp64 tensor pipe:
+    // 8 x 8 output tiles over the 16 warps, accumulated across the tiles
+    const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+    const int nt = (p + 7) >> 3;
+    double hacc[4][4][2];   // [tile][chain]: 4 independent k-step chains per tile
 #pragma unroll
-    for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) hacc[t] = 0.0;
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) hacc[q][c][0] = hacc[q][c][1] = 0.0;
     for (int64_t i0 = int64_t(crank) * kTileRows; i0 < n; i0 += kCluster * kTileRows) {
       const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
       load_tile(i0, rows);
       __syncthreads();
       RITZ_STAMP(0);
 #pragma unroll
-      for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) {
-        const int e = tid + t * kThreads;
-        if (e >= p * p) break;
-        const int i = e / p, j = e % p;
-        const double* qi = Qs + i * LDT;
-        const double* zj = Zs + j * LDT;
-        double a = hacc[t];
-        for (int r = 0; r < kTileRows; ++r) a = fma(qi[r], zj[r], a);
-        hacc[t] = a;
+      for (int q = 0; q < 4; ++q) {
+        const int t = warp + 16 * q;
+        if (t >= nt * nt) break;
+        const double* qa = Qs + (8 * (t / nt) + fr) * LDT + fk;
+        const double* zb = Zs + (8 * (t % nt) + fr) * LDT + fk;
+#pragma unroll
+        for (int r0 = 0; r0 < kTileRows; r0 += 16)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dmma(hacc[q][c], qa[r0 + 4 * c], zb[r0 + 4 * c]);
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int t = 0; t < kMaxP * kMaxP / kThreads; ++t) {
-      const int e = tid + t * kThreads;
-      if (e < p * p) Hp[(e / p) * LDS + e % p] = hacc[t];
+    for (int q = 0; q < 4; ++q) {
+      const int t = warp + 16 * q;
+      if (t >= nt * nt) break;
+      const int row = 8 * (t / nt) + fr;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * (t % nt) + 2 * fk + h;
+        const double v = (hacc[q][0][h] + hacc[q][1][h]) + (hacc[q][2][h] + hacc[q][3][h]);
+        if (row < p && col < p) Hp[row * LDS + col] = v;
+      }
     }
     RITZ_STAMP(1);
     cluster.sync();
@@ -298,18 +363,22 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
         if (clamp) atomicOr(&s_clamp, 1);
       }
       __syncthreads();
+      if (itn == 0) RITZ_STAMP(16);
       if (s_red[1] <= floor_abs || s_clamp) break;
       ++newton;
-      small_mm<false, 0>(V, S, W, P, tid);   // W = V (I + E)
+      dmma_mm_rt(V, S, W, P, tid, false, 0);   // W = V (I + E)
       __syncthreads();
-      small_mm<true, 1>(W, W, S, P, tid);    // S = 1.5 I - 0.5 W^T W
+      if (itn == 0) RITZ_STAMP(17);
+      dmma_mm_rt(W, W, S, P, tid, true, 1);    // S = 1.5 I - 0.5 W^T W
       __syncthreads();
-      small_mm<false, 0>(W, S, V, P, tid);   // V = W S
+      if (itn == 0) RITZ_STAMP(18);
+      dmma_mm_rt(W, S, V, P, tid, false, 0);   // V = W S
       __syncthreads();
-      small_mm<false, 0>(H, V, W, P, tid);   // W = H V
+      dmma_mm_rt(H, V, W, P, tid, false, 0);   // W = H V
       __syncthreads();
-      small_mm<true, 0>(V, W, smr, P, tid);  // A = V^T H V
+      dmma_mm_rt(V, W, smr, P, tid, true, 0);  // A = V^T H V
       __syncthreads();
+      if (itn == 0) RITZ_STAMP(19);
       for (int e = tid; e < P * P; e += kThreads) {
         const int i = e / P, j = e % P;
         if (i < j) {
@@ -319,6 +388,7 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
         }
       }
       __syncthreads();
+      if (itn == 0) RITZ_STAMP(20);
     }
     RITZ_STAMP(4);
     int cur = 0;
@@ -457,19 +527,42 @@ ritz_kernel(const double* __restrict__ q, int64_t ldq, const double* __restrict_
     const int rows = n - i0 < kTileRows ? int(n - i0) : kTileRows;
     load_tile(i0, rows);
     __syncthreads();
+    {  // U_t = Q_t V_r, Y_t = Z_t V_r on the fp64 tensor pipe -> Us / Yv
+      const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+      const int ntj = (rank + 7) >> 3;
+      for (int t = warp; t < 2 * 8 * ntj; t += kThreads / 32) {
+        const int which = t / (8 * ntj), rem = t % (8 * ntj), mt = rem / ntj, nj = rem % ntj;
+        const double* src = which ? Zs : Qs;
+        const int i = 8 * mt + fr, j = 8 * nj + fr;
+        double c[8][2];     // k-step s -> chain s % 8 (independent DMMAs)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+        for (int l0 = 0; l0 < p; l0 += 32) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int l = l0 + 4 * q + fk;
+            dmma(c[q], l < p ? src[l * LDT + i] : 0.0, l < p ? Vs[l * LDS + j] : 0.0);
+          }
+        }
+        double* dst = which ? Yv : Us;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * nj + 2 * fk + h;
+          double v = 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v += c[q][h];
+          if (col < rank) dst[i * LDS + col] = v;
+        }
+      }
+    }
+    __syncthreads();
     if (g < ngroups) {
       const int j0 = 8 * g;
       double u[8], y[8];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) u[jj] = y[jj] = 0.0;
-      for (int l = 0; l < p; ++l) {
-        const double q = Qs[l * LDT + r], z = Zs[l * LDT + r];
-        const double* vr = Vs + l * LDS + j0;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          u[jj] = fma(q, vr[jj], u[jj]);
-          y[jj] = fma(z, vr[jj], y[jj]);
-        }
+      for (int jj = 0; jj < 8; ++jj) {
+        u[jj] = j0 + jj < rank ? Us[r * LDS + j0 + jj] : 0.0;
+        y[jj] = j0 + jj < rank ? Yv[r * LDS + j0 + jj] : 0.0;
       }
       if (r < rows) {
         const int64_t i = i0 + r;

@@ -672,7 +672,7 @@ int sbt_trace_dump(int which, long long* out) {
 // diagnostics build only (tools/ritz_probe.py with SBT_LIB): the Ritz
 // kernel's phase stamps of the last launch
 int sbt_ritz_clock(long long* out) {
-  return cudaMemcpyFromSymbol(out, sbt::ritz::g_ritz_clock, 16 * sizeof(long long)) ==
+  return cudaMemcpyFromSymbol(out, sbt::ritz::g_ritz_clock, 24 * sizeof(long long)) ==
                  cudaSuccess ? 0 : -3;
 }
 int sbt_ga_clock(long long* out) {

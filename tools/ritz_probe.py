@@ -34,7 +34,7 @@ for n, p, warm in ((512, 32, True), (512, 48, True), (512, 32, False), (512, 48,
     e1.record(); torch.cuda.synchronize()
     print(f"n={n} p={p} warm={warm}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us, sweeps {rel[1].item():.0f}, rel {rel[0].item():.1e}, cycles {rel[2:].tolist()}")
     if hasattr(lib, "sbt_ritz_clock"):   # SBT_LIB = a -DSBT_RITZ_CLOCK build
-        clk = (ctypes.c_longlong * 16)()
+        clk = (ctypes.c_longlong * 24)()
         call(); torch.cuda.synchronize()
         lib.sbt_ritz_clock(clk)
-        print("   stamps (cycles since start, CTA 0):", list(clk)[:12])
+        print("   stamps (cycles since start, CTA 0):", list(clk)[:12], "newton it0:", list(clk)[16:21])

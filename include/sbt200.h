@@ -55,6 +55,13 @@ const char* sbt_last_kernel(void);
 /* Force a kernel family: 0 = auto, 1 = generic SIMT, 2 = tensor-core tiled,
    3 = small-matrix batched.  Used by tests to cover every path. */
 int sbt_set_kernel_override(int which);
+/* fp32 accumulation mode of the narrow (N <= 64) tensor-core tiles for the
+   calling thread: 1 = unbiased (default: round-to-nearest TF32 split, step
+   accumulators summed in round-to-nearest fp32), 0 = fast (the tensor core's
+   truncating accumulator: a relative shrink of ~K/16 ulp, harmless where only
+   directions matter, e.g. the HOOI factor-update products).  Returns the
+   previous mode. */
+int sbt_set_accumulation(int mode);
 
 /* Diagnostics (not part of the reference seam): measured fp64 throughput in
    TFLOP/s of the DMMA tensor pipe (kind 0) or DFMA SIMT pipe (kind 1). */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "sbt_launch_count": ([], c_int64),
     "sbt_last_kernel": ([], ctypes.c_char_p),
     "sbt_set_kernel_override": ([c_int], c_int),
+    "sbt_set_accumulation": ([c_int], c_int),
     "sbt_probe_fp64_peak": ([c_int, ctypes.POINTER(c_double)], c_int),
     "sbt_probe_tf32_peak": ([ctypes.POINTER(c_double)], c_int),
     "sbt_probe_tf32_sustained": ([c_double, ctypes.POINTER(c_double)], c_int),
@@ -147,6 +148,20 @@ def set_kernel_override(which) -> None:
     names = {"auto": 0, "generic": 1, "tensor": 2, "small": 3}
     which = names.get(which, which)
     check(load().sbt_set_kernel_override(int(which)), "sbt_set_kernel_override")
+
+
+class fast_accumulation:
+    """Context manager: narrow fp32 tensor-core tiles launched by this thread
+    inside the block use the fast (truncating) accumulator instead of the
+    unbiased default (``sbt_set_accumulation``)."""
+
+    def __enter__(self):
+        self.prev = load().sbt_set_accumulation(0)
+        return self
+
+    def __exit__(self, *exc):
+        load().sbt_set_accumulation(self.prev)
+        return False
 
 
 def probe_fp64_peak(kind: str = "dmma") -> float:

@@ -45,6 +45,8 @@ void note_launch(const char* name) {
 }
 
 int kernel_override() { return g_override.load(std::memory_order_relaxed); }
+static thread_local int t_accumulation = 1;
+int accumulation_mode() { return t_accumulation; }
 
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(SBT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -370,6 +372,11 @@ int sbt_set_kernel_override(int which) {
   if (which < 0 || which > 3) return SBT_EINVAL;
   g_override.store(which);
   return SBT_OK;
+}
+int sbt_set_accumulation(int mode) {
+  const int prev = t_accumulation;
+  t_accumulation = mode ? 1 : 0;
+  return prev;
 }
 
 // Diagnostics: measured fp64 tensor (kind 0 = DMMA) or SIMT (kind 1 = DFMA)

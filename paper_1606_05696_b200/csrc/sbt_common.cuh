@@ -33,6 +33,7 @@ int set_smem_attr(const void* fn, int bytes);
 // record a CUDA failure of a launcher for sbt_last_error(); returns SBT_ECUDA
 int cuda_fail(cudaError_t e, const char* what);
 int kernel_override();  // 0 auto, 1 generic, 2 tensor-core tiled, 3 small-matrix
+int accumulation_mode();  // this thread's sbt_set_accumulation (1 unbiased, 0 fast)
 constexpr int kNumSMs = 148;
 
 __host__ __device__ constexpr int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -213,7 +213,7 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
   // narrow tiles run the unbiased FLUSH mode (k_tf32x3_pair_tma.cuh header),
   // which keeps the cross terms in the split accumulator
   static const int narrow_flush = env_int("SBT_TC_FLUSH", 1);
-  if (narrow_flush && out->bnt <= 64) out->split = true;
+  if (narrow_flush && accumulation_mode() && out->bnt <= 64) out->split = true;
   // split accumulators (K > 512) fill TMEM at 256 columns: 128-wide tiles keep
   // them double-buffered, so the epilogue overlaps the next tile's MMAs
   static const int split_bnt = env_int("SBT_TC_SPLIT_BNT", 256);

@@ -406,8 +406,18 @@ def _mode_product_acc64(cur: DenseTensor, u, r: int) -> DenseTensor:
     return out
 
 
-def _mode_product(cur: DenseTensor, u, r: int, transpose: bool) -> DenseTensor:
-    """One planned contraction T x_r U^T (transpose) or T x_r U."""
+def _mode_product(cur: DenseTensor, u, r: int, transpose: bool,
+                  fast: bool = False) -> DenseTensor:
+    """One planned contraction T x_r U^T (transpose) or T x_r U.  ``fast``:
+    the product only feeds a factor update (an eigenvector direction, blind to
+    the ~K/16-ulp uniform shrink of the tensor core's truncating fp32
+    accumulator), so the narrow tiles may skip the unbiased accumulation that
+    the products feeding the core -- whose norm the fit compares with ||T|| --
+    need (sbt_set_accumulation)."""
+    if fast:
+        from . import _lib
+        with _lib.fast_accumulation():
+            return _mode_product(cur, u, r, transpose)
     order = cur.layout.order
     torch = _torch()
     if (transpose and cur.dtype == torch.float32 and cur.layout.is_packed()
@@ -479,7 +489,8 @@ def _as_factor_tensor(u, dtype, device=None):
     return DenseTensor(Layout.packed(tuple(u.shape)), flat)
 
 
-def _mode_product_chain(t: DenseTensor, factors, skip, transpose: bool) -> DenseTensor:
+def _mode_product_chain(t: DenseTensor, factors, skip, transpose: bool,
+                        fast: bool = False) -> DenseTensor:
     """Apply U_r^T (transpose) or U_r along every mode except ``skip``, one
     planned contraction per mode, larger reduction extent first
     (reference tucker.py:87-123)."""
@@ -489,7 +500,7 @@ def _mode_product_chain(t: DenseTensor, factors, skip, transpose: bool) -> Dense
     modes.sort(key=lambda r: -red(r))
     cur = t
     for r in modes:
-        cur = _mode_product(cur, factors[r], r, transpose)
+        cur = _mode_product(cur, factors[r], r, transpose, fast)
     return cur
 
 
@@ -520,13 +531,16 @@ def _hooi_sweep(t: DenseTensor, factors, fast: bool, factor_fn) -> DenseTensor:
     """One HOOI iteration (tucker.py:160-167): update every factor in place via
     factor_fn(y, r, warm) and return the core G = T x_1 U_1^T ... x_N U_N^T."""
     order = t.layout.order
+    # products that only feed a factor update run with the fast accumulator;
+    # those feeding the core (X0, its mode-1 product, the core itself) keep
+    # the unbiased one (see _mode_product)
     if fast:
         # skip=0 chain: modes 1, 2 (reference order); then X0 = T x_0 U_0^T
-        y = _mode_product_chain(t, factors, skip=0, transpose=True)
+        y = _mode_product_chain(t, factors, skip=0, transpose=True, fast=True)
         factors[0] = factor_fn(y, 0, factors[0])
         x0 = _mode_product(t, factors[0], 0, True)
         # reference skip=1 chain is [0, 2] and skip=2 chain is [0, 1]
-        y = _mode_product(x0, factors[2], 2, True)
+        y = _mode_product(x0, factors[2], 2, True, fast=True)
         factors[1] = factor_fn(y, 1, factors[1])
         y2 = _mode_product(x0, factors[1], 1, True)
         factors[2] = factor_fn(y2, 2, factors[2])
@@ -535,7 +549,7 @@ def _hooi_sweep(t: DenseTensor, factors, fast: bool, factor_fn) -> DenseTensor:
             return _mode_product(y2, factors[2], 2, True)
         return _mode_product(_mode_product(x0, factors[2], 2, True), factors[1], 1, True)
     for r in range(order):
-        y = _mode_product_chain(t, factors, skip=r, transpose=True)
+        y = _mode_product_chain(t, factors, skip=r, transpose=True, fast=True)
         factors[r] = factor_fn(y, r, factors[r])
     return tucker_core(t, factors)
 

@@ -6,7 +6,7 @@
 #include <cstdio>
 #include <vector>
 #include "../paper_1606_05696_b200/csrc/sbt_common.cuh"
-namespace sbt { void note_launch(const char*) {} int kernel_override() { return 0; } }
+namespace sbt { void note_launch(const char*) {} int kernel_override() { return 0; } int accumulation_mode() { return 1; } }
 #include "../paper_1606_05696_b200/csrc/sbt_dispatch.cuh"
 using namespace sbt;
 int main(int argc, char** argv) {

@@ -310,9 +310,12 @@ def tensor_peak(dtype_name, sustained=False):
         return FP64_NOMINAL_TFLOPS, "fp64 DMMA nominal (datasheet 37 TFLOP/s)"
 
 
-def roofline_obj(flops, nbytes, ms, tpeak, tnote, hbm, kernel, traffic_key, extra=None):
+def roofline_obj(flops, nbytes, ms, tpeak, tnote, hbm, kernel, traffic_key, extra=None,
+                 traffic_scale=1):
     """roofline of one kernel: bound = the slower of tensor pipe at peak and
-    algorithmic bytes at HBM bandwidth; achieved in the bound's unit."""
+    algorithmic bytes at HBM bandwidth; achieved in the bound's unit.
+    traffic_scale: the ncu capture covers one of that many identical launches
+    that the timed "launch" stands for (fp64 sweep: one DMMA launch per case)."""
     t_tensor = flops / (tpeak * 1e12)
     t_hbm = nbytes / (hbm * 1e9)
     bound = "tensor" if t_tensor >= t_hbm else "hbm"
@@ -322,7 +325,9 @@ def roofline_obj(flops, nbytes, ms, tpeak, tnote, hbm, kernel, traffic_key, extr
         achieved, peak, unit = nbytes / (ms * 1e-3) / 1e9, hbm, "GB/s"
     out = {"bound": bound, "kernel": kernel, "achieved": round(achieved, 3),
            "peak": round(peak, 2), "unit": unit, "frac": round(achieved / peak, 4),
-           "traffic": ncu_traffic(traffic_key), "peak_source": tnote if bound == "tensor" else
+           "traffic": (ncu_traffic(traffic_key) * traffic_scale
+                       if ncu_traffic(traffic_key) is not None else None),
+           "peak_source": tnote if bound == "tensor" else
            load_peaks()["source"], "launch_ms": round(ms, 4),
            "algorithmic": {"flop": flops, "bytes": nbytes},
            "hbm_achieved_gbs": round(nbytes / (ms * 1e-3) / 1e9, 1), "hbm_peak_gbs": hbm,
@@ -509,8 +514,16 @@ def run_sweep(args, ctx):
     hbm = load_peaks().get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     dom = max(fam, key=lambda k: fam[k]["ms"])
     d = fam[dom]
+    # fp32 groups are ONE persistent launch over all their cases; fp64 groups
+    # are one DMMA launch per case (forked over streams): the committed ncu
+    # capture is then of one case's launch
+    per_case_launch = not d["kernel"].startswith("tc_tf32x3_pair")
     roof = roofline_obj(d["cases"] * fl, d["cases"] * by, d["ms"], tpeak, tnote, hbm,
-                        d["kernel"], f"{d['kernel']}/n{n}/{args.dtype}", extra={
+                        d["kernel"], f"{d['kernel']}/n{n}/{args.dtype}",
+                        traffic_scale=d["cases"] if per_case_launch else 1, extra={
+                            "traffic_note": ("ncu dram bytes of one case's launch x the cases"
+                                             if per_case_launch else
+                                             "ncu dram bytes of the grouped launch"),
                             "per_launch_cases": d["cases"],
                             "kernel_share_of_step": round(d["ms"] / sum(
                                 f["ms"] for f in fam.values()), 4),
@@ -880,7 +893,7 @@ def run_hooi(args, ctx):
     """configs[3]: HOOI of a synthetic 512^3 tensor, rank 32, fp32.  A step is
     one HOOI iteration; ms per iteration = difference of a (1+2K)- and a
     (1+K)-iteration run (both pay the HOSVD init, the graph capture and the
-    final core), best of 3."""
+    final core), best of 3, each run timed with CUDA events on its stream."""
     import gc
 
     import torch
@@ -904,10 +917,13 @@ def run_hooi(args, ctx):
         try:
             torch.cuda.synchronize()
             n0 = _lib.launch_count()
-            t0 = time.perf_counter()
+            stream = torch.cuda.current_stream(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             m = sbt.hooi(t, (r, r, r), max_iters=k, tol=-1.0)
+            e1.record(stream)
             torch.cuda.synchronize()
-            return time.perf_counter() - t0, m, _lib.launch_count() - n0
+            return e0.elapsed_time(e1) * 1e-3, m, _lib.launch_count() - n0
         finally:
             gc.enable()
 
@@ -998,10 +1014,14 @@ def run_hooi_sharded(args, ctx, n, r, dtype):
     def run(k):
         torch.cuda.synchronize()
         ctx.barrier()
-        t0 = time.perf_counter()
-        out = hooi_sharded(local, (n, n, n), (r, r, r), max_iters=k, tol=-1.0)
         torch.cuda.synchronize()
-        return ctx.max_over_ranks(time.perf_counter() - t0), out
+        stream = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = hooi_sharded(local, (n, n, n), (r, r, r), max_iters=k, tol=-1.0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return ctx.max_over_ranks(e0.elapsed_time(e1) * 1e-3), out
 
     with ClockSampler(dev.index) as clocks:
         t1 = min(run(1)[0] for _ in range(2))

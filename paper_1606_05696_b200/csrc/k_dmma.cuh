@@ -43,6 +43,9 @@ constexpr int LDBB = 148;
 constexpr int TILE_RAW = 128 * LDK > BK * LDMN ? 128 * LDK : BK * LDMN;  // BK 16: 2560 vs 2112
 constexpr int TILE_DOUBLES = TILE_RAW > BK * LDBB ? TILE_RAW : BK * LDBB;
 constexpr int SMEM_BYTES = STAGES * 2 * TILE_DOUBLES * 8;                   // 120 KB
+// BNT = 64 tiles: the B half is 64 x BK (K-major) or BK x LDMN (MN-major)
+constexpr int B64_DOUBLES = 64 * LDK > BK * LDMN ? 64 * LDK : BK * LDMN;
+constexpr int SMEM_BYTES_N64 = STAGES * (TILE_DOUBLES + B64_DOUBLES) * 8;   // 109.5 KB at BK 16
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -71,12 +74,12 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // Stage one operand tile (rows = MN extent 128, k = 16) with 16-byte cp.async.
 // KMAJ: global k unit-stride -> smem [mn][LDK]; else mn unit-stride -> [k][LDMN].
-template <bool KMAJ, int NT = kThreads>
+template <bool KMAJ, int NT = kThreads, int ROWS = 128>
 __device__ __forceinline__ void stage_operand(double* dst, const double* __restrict__ src,
                                               int64_t mn0, int64_t k0, int64_t mn_ext,
                                               int64_t k_ext, int64_t s_mn, int64_t s_k, int tid) {
 #pragma unroll
-  for (int i = 0; i < 64 * BK / NT; ++i) {  // 128 x BK doubles in 16-byte chunks
+  for (int i = 0; i < ROWS * BK / 2 / NT; ++i) {  // ROWS x BK doubles in 16-byte chunks
     const int e = tid + i * NT;
     if (KMAJ) {
       const int mn = e / (BK / 2), k2 = (e % (BK / 2)) * 2;
@@ -84,7 +87,7 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
       const bool ok = gm < mn_ext && gk < k_ext;
       cp_async16(dst + mn * LDK + k2, ok ? src + gm * s_mn + gk : src, ok);
     } else {
-      const int k = e >> 6, mn2 = (e & 63) * 2;
+      const int k = e / (ROWS / 2), mn2 = (e % (ROWS / 2)) * 2;
       const int64_t gm = mn0 + mn2, gk = k0 + k;
       const bool ok = gm < mn_ext && gk < k_ext;
       cp_async16(dst + k * LDMN + mn2, ok ? src + gm + gk * s_k : src, ok);
@@ -107,11 +110,17 @@ __device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__
   }
 }
 
-template <bool A_K, bool B_K, bool BB = false, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 1)
+// BNT: N extent of the CTA tile.  128 (one CTA per SM; NW = 8 or 16); 64
+// with NW = 8 (4 x 2 warps of 32 x 32, <= 128 registers) runs two CTAs per
+// SM, so one CTA's prologue / epilogue overlaps the other's main loop.
+template <bool A_K, bool B_K, bool BB = false, int NW = 8, int BNT = 128>
+__global__ void __launch_bounds__(NW * 32, BNT == 64 ? 2 : 1)
 dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   extern __shared__ __align__(16) double sm[];
-  constexpr int NT = NW * 32, WM = WarpGrid<NW>::WM, TM = WarpGrid<NW>::TM;
+  static_assert(BNT == 128 || (BNT == 64 && NW == 8), "tile configurations");
+  constexpr int NT = NW * 32;
+  constexpr int WN = BNT / 32;                       // warps along N (32 columns each)
+  constexpr int WM = NW / WN, TM = 128 / WM / 8;     // warps along M, DMMA row tiles per warp
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp % WM, wn = warp / WM;  // WM x 4 warps
@@ -119,7 +128,7 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   int64_t t = blockIdx.x;
   const int64_t m0 = (t % tiles_m) * (BB ? 32 : BM);
   t /= tiles_m;
-  const int64_t n0 = (t % tiles_n) * BN;
+  const int64_t n0 = (t % tiles_n) * BNT;
   t /= tiles_n;
   const int64_t nbatch = BB ? (p.batch + 3) / 4 : p.batch;
   const int64_t pb = t % nbatch, qb = t / nbatch;
@@ -127,15 +136,16 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   const double* __restrict__ B = p.b + (BB ? 0 : pb * p.bps) + qb * p.bps2;
   const int nkb = int((p.k + BK - 1) / BK);
 
+  constexpr int STAGE_D = TILE_DOUBLES + (BNT == 128 ? TILE_DOUBLES : B64_DOUBLES);
   auto stage = [&](int kb) {
-    double* sa = sm + (kb % STAGES) * 2 * TILE_DOUBLES;
+    double* sa = sm + (kb % STAGES) * STAGE_D;
     double* sb = sa + TILE_DOUBLES;
     const int64_t k0 = int64_t(kb) * BK;
     if (BB)
       stage_bb<NT>(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
     else
       stage_operand<A_K, NT>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
-    stage_operand<B_K, NT>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
+    stage_operand<B_K, NT, BNT>(sb, B, n0, k0, p.n, p.k, B_K ? p.bcs : 1, B_K ? 1 : p.brs, tid);
   };
 
   double acc[TM][4][2];
@@ -155,7 +165,7 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
     __syncthreads();
     if (kb + STAGES - 1 < nkb) stage(kb + STAGES - 1);
     cp_async_commit();
-    const double* sa = sm + (kb % STAGES) * 2 * TILE_DOUBLES;
+    const double* sa = sm + (kb % STAGES) * STAGE_D;
     const double* sb = sa + TILE_DOUBLES;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {

@@ -439,14 +439,16 @@ static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm
   return true;
 }
 
-template <bool AK, bool BK_, bool BB, int NW>
+template <bool AK, bool BK_, bool BB, int NW, int BNT = 128>
 static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
-  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW>;
-  if (set_smem_attr(reinterpret_cast<const void*>(kern), dmma::SMEM_BYTES) != 0) return -3;
-  const int64_t tiles_m = ceil_div(p.m, BB ? 32 : dmma::BM), tiles_n = ceil_div(p.n, dmma::BN);
+  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW, BNT>;
+  // BNT = 64: the B tile is half as wide (two CTAs per SM need <= 113 KB each)
+  const int smem = BNT == 128 ? dmma::SMEM_BYTES : dmma::SMEM_BYTES_N64;
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), smem) != 0) return -3;
+  const int64_t tiles_m = ceil_div(p.m, BB ? 32 : dmma::BM), tiles_n = ceil_div(p.n, BNT);
   const int64_t total = tiles_m * tiles_n * (BB ? ceil_div(p.batch, 4) : p.batch) * p.batch2;
   if (total > int64_t(0x7fffffff)) return -2;
-  kern<<<dim3(unsigned(total)), dim3(NW * 32), dmma::SMEM_BYTES, stream>>>(p, tiles_m, tiles_n);
+  kern<<<dim3(unsigned(total)), dim3(NW * 32), smem, stream>>>(p, tiles_m, tiles_n);
   note_launch(BB ? "tc_dmma_f64_bb" : "tc_dmma_f64");
   return 1;
 }
@@ -459,6 +461,8 @@ static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
 template <bool AK, bool BK_, bool BB = false>
 static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   static const int nw_env = env_int("SBT_DMMA_WARPS", 0);  // 0 = by K
+  static const int bn_env = env_int("SBT_DMMA_BN", 128);   // 64: two CTAs per SM
+  if (bn_env == 64) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   const int nw = nw_env ? nw_env : (p.k <= 256 ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
                   : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);

@@ -95,8 +95,8 @@ class DeviceOps:
         from . import tucker as tk
         self.tk = tk
 
-    def mode_product(self, x, u, mode):
-        return self.tk._mode_product(x, u, mode, True)
+    def mode_product(self, x, u, mode, fast=False):
+        return self.tk._mode_product(x, u, mode, True, fast)
 
     def gram(self, x, r):
         return self.tk.gram_of_unfolding(x, r)
@@ -151,7 +151,7 @@ class HostOps(DeviceOps):
         from . import tucker as tk
         self.tk = tk
 
-    def mode_product(self, x, u, mode):
+    def mode_product(self, x, u, mode, fast=False):
         import torch
         from .layout import DenseTensor
         v = x.view()
@@ -267,13 +267,14 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
     def local_u2(u2):
         return u2[c0:c1]
 
-    def chain(factors, skip):
+    def chain(factors, skip, fast=False):
         """Reference product order (tucker.py:95-99: larger reduction extent
-        first, ties ascending) on the slab; the collective at the end."""
+        first, ties ascending) on the slab; the collective at the end.  fast:
+        the result only feeds a factor update (tucker._mode_product)."""
         modes = sorted((m for m in range(3) if m != skip), key=lambda m: -full_dims[m])
         cur, partial = t_local, False
         for m in modes:
-            cur = ops.mode_product(cur, local_u2(factors[m]) if m == 2 else factors[m], m)
+            cur = ops.mode_product(cur, local_u2(factors[m]) if m == 2 else factors[m], m, fast)
             partial = partial or m == 2
         return allreduce(cur) if partial else allgather_last(cur)
 
@@ -288,10 +289,10 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
     def sweep(factors, factor_fn):
         """One iteration (tucker.py:160-167); returns the core (replicated)."""
         if reuse:
-            y = chain(factors, 0)
+            y = chain(factors, 0, fast=True)
             factors[0] = factor_fn(y, 0, factors[0])
             x0 = ops.mode_product(t_local, factors[0], 0)
-            y = allreduce(ops.mode_product(x0, local_u2(factors[2]), 2))
+            y = allreduce(ops.mode_product(x0, local_u2(factors[2]), 2, fast=True))
             factors[1] = factor_fn(y, 1, factors[1])
             y2 = allgather_last(ops.mode_product(x0, factors[1], 1))
             factors[2] = factor_fn(y2, 2, factors[2])
@@ -300,7 +301,7 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
             g = allreduce(ops.mode_product(x0, local_u2(factors[2]), 2))
             return ops.mode_product(g, factors[1], 1)
         for r in range(3):
-            factors[r] = factor_fn(chain(factors, r), r, factors[r])
+            factors[r] = factor_fn(chain(factors, r, fast=True), r, factors[r])
         return chain(factors, None)
 
     fits, prev, iters = [], -np.inf, 0

@@ -461,8 +461,13 @@ static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
 template <bool AK, bool BK_, bool BB = false>
 static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   static const int nw_env = env_int("SBT_DMMA_WARPS", 0);  // 0 = by K
-  static const int bn_env = env_int("SBT_DMMA_BN", 128);   // 64: two CTAs per SM
-  if (bn_env == 64) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
+  // plain tiles: 128 x 64 with two CTAs per SM (one CTA's cp.async prologue and
+  // C epilogue overlap the other's DMMA loop).  Measured (36-case fp64 sweep,
+  // plain-case launches, 128 -> 64): n=128 24.7 -> 26.8, n=256 28.6 -> 30.3
+  // TF/s; the batch-blocked tiles lose (25.0 -> 23.4) and keep 128 x 128.
+  static const int bn_env = env_int("SBT_DMMA_BN", 0);     // 0 = by tile kind
+  const int bn = bn_env ? bn_env : (BB ? 128 : 64);
+  if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   const int nw = nw_env ? nw_env : (p.k <= 256 ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
                   : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);

@@ -586,6 +586,27 @@ static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
 }
 
 // fp32 64 x 64 x 64 batches with column-major A, B and C: 8 x 8 register blocks.
+// fp32 n = 64 on the tensor pipe (k_small64.cuh small64_mma_kernel); 0 = not
+// eligible (then the FFMA kernel below).  SBT_SMALL64_MMA=0 keeps the FFMA one.
+static int try_small64_mma(const GemmParams<float>& p, cudaStream_t stream) {
+  using namespace small64mma;
+  static const int on = env_int("SBT_SMALL64_MMA", 1);
+  if (!on) return 0;
+  if (set_smem_attr(reinterpret_cast<const void*>(small64_mma_kernel), SMEM_BYTES) != 0)
+    return -3;
+  CUtensorMap ta, tb;
+  if (!make_tmap_f32(&ta, p.a, 64, 64, 64, p.batch, p.aps, 1, 0, LDA, 64,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, 1) ||
+      !make_tmap_f32(&tb, p.b, 64, 64, 64, p.batch, p.bps, 1, 0, LDB, 64,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, 1))
+    return 0;
+  const int64_t cap = int64_t(kNumSMs) * CTAS_PER_SM;
+  const int64_t grid = p.batch < cap ? p.batch : cap;
+  small64_mma_kernel<<<dim3(unsigned(grid)), dim3(kThreads), SMEM_BYTES, stream>>>(p, ta, tb);
+  note_launch("small64_mma_f32");
+  return 1;
+}
+
 static int try_small64(const GemmParams<float>& p, cudaStream_t stream) {
   using namespace small64;
   if (p.m != 64 || p.n != 64 || p.k != 64) return 0;
@@ -594,6 +615,10 @@ static int try_small64(const GemmParams<float>& p, cudaStream_t stream) {
   if (p.aps % 4 || p.bps % 4 || p.aps < 4096 || p.bps < 4096 || !aligned16(p.a) ||
       !aligned16(p.b) || p.batch > (int64_t(1) << 31))
     return 0;
+  {
+    const int rc = try_small64_mma(p, stream);
+    if (rc != 0) return rc;
+  }
   if (set_smem_attr(reinterpret_cast<const void*>(small64_kernel), SMEM_BYTES) != 0) return -3;
   CUtensorMap ta, tb;
   if (!make_tmap_f32(&ta, p.a, 64, 64, 64, p.batch, p.aps, 1, 0, 64, 64,

@@ -962,17 +962,22 @@ def test_grouped_execution_rejects_dependent_calls():
         sbt.execute_plans([(plan, a, b, 1.0, 0.0, c), (plan, a, b, 1.0, 0.0, c)])
 
 
-@pytest.mark.parametrize("P,beta", [(2001, 0.0), (999, 0.5)])
-def test_small64_fp32_register_blocked(P, beta):
-    """fp32 64^3 batches take the 8x8-register-blocked kernel (odd batch: last
-    group half full; beta != 0 takes the read-modify-write path)."""
+@pytest.mark.parametrize("P,beta,mma", [(2001, 0.0, 1), (999, 0.5, 1), (2001, 0.0, 0),
+                                        (999, 0.5, 0)])
+def test_small64_fp32(P, beta, mma, monkeypatch):
+    """fp32 64^3 batches: the mma.sync 3xTF32 kernel (default) or, with
+    SBT_SMALL64_MMA=0 in the environment (read once by the library), the
+    8x8-register-blocked FFMA kernel -- odd batch, beta != 0."""
     n = 64
+    import os
+    if mma != (os.environ.get("SBT_SMALL64_MMA", "1") != "0"):
+        pytest.skip("variant selected by SBT_SMALL64_MMA (tools/check_small64.sh runs both)")
     rng = np.random.default_rng(P)
     ha, hb, hc = (rng.uniform(-1, 1, n * n * P) for _ in range(3))
     a, b, c = dev(ha, torch.float32), dev(hb, torch.float32), dev(hc, torch.float32)
     kernels.strided_batched_gemm("N", "N", n, n, n, 1.5, a, n, n * n, b, n, n * n, beta, c, n,
                                  n * n, P)
-    assert _lib.last_kernel() == "small64_f32"
+    assert _lib.last_kernel() == ("small64_mma_f32" if mma else "small64_f32")
     A = host(a).reshape(P, n, n).transpose(0, 2, 1)
     B = host(b).reshape(P, n, n).transpose(0, 2, 1)
     want = (1.5 * (A @ B)).transpose(0, 2, 1).reshape(-1) + beta * host(dev(hc, torch.float32))

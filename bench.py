@@ -949,7 +949,10 @@ def run_hooi(args, ctx):
                       "parallelism": "single GPU", "l2": f"T = {it * n ** 3 / 1e6:.0f} MB > L2"}
     line["roofline"] = {"bound": "hbm", "achieved": round(nbytes / per_iter / 1e9, 1),
                         "peak": hbm, "unit": "GB/s",
-                        "frac": round(nbytes / (hbm * 1e9) / per_iter, 4), "traffic": None,
+                        "frac": round(nbytes / (hbm * 1e9) / per_iter, 4),
+                        "traffic": ncu_traffic(f"hooi_iteration/n{n}/{args.dtype}"),
+                        "traffic_note": "ncu dram bytes of one iteration's launches "
+                                        "(profiles/r02_ncu_hooi_iter.csv)",
                         "kernel": "HOOI iteration (CUDA graph)",
                         "algorithmic_bytes_per_iter": nbytes,
                         "floor_ms_per_iter": round(nbytes / (hbm * 1e9) * 1e3, 4),

@@ -481,8 +481,10 @@ def run_sweep(args, ctx):
         kernel_of[cid] = _lib.last_kernel()
     # per-case attribution (events between launches, no graph)
     per_case = {}
-    for cid, plan, a, b, c in work:
-        per_case[cid] = event_ms(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), 3, dev)
+    for cid, plan, a, b, c in work:   # device time of one call (graph replay: no host gaps)
+        g1, _ = capture(lambda: execute_plan(plan, a, b, 1.0, 0.0, c), dev)
+        per_case[cid] = event_ms(g1.replay, 5, dev)
+        del g1
     fl, by = flops_bytes(n, itemsize)
     # dominant kernel: one grouped launch per subset, event-timed on its stream
     fam = {}

@@ -42,8 +42,8 @@
 // truncated, so the residual that the tensor core truncates again is always of
 // x's sign -- every operand is shrunk by ~2^-22 on average; (2) the main
 // accumulator is truncated on every MMA, a shrink of ~K/16 ulp for coherent
-// sums.  FLUSH removes both: the converters write hi = rna_tf32(x) in place
-// and lo = rna_tf32(x - hi) (signs now independent of x), and the hi*hi MMA of
+// sums.  FLUSH removes both: the converters write lo = rna_tf32(x - trunc(x))
+// (the rounding of the residual is now unbiased), and the hi*hi MMA of
 // every group of G K=8 steps writes a FRESH TMEM step accumulator (8 rotating
 // slots) that the epilogue warps add into registers in round-to-nearest fp32,
 // in k order; the 2^-11-sized cross terms keep their own accumulator.  The
@@ -471,14 +471,17 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
             ptx::sts_v4(lo_base + Gm::SLOT_BYTES + off, __float_as_uint(v[i].x),
                         __float_as_uint(v[i].y), __float_as_uint(v[i].z), __float_as_uint(v[i].w));
           }
-          if constexpr (FLUSH) {  // unbiased split, hi written back in place
-            uint32_t h[4], l[4];
-            ptx::split_tf32(v[i].x, h[0], l[0]);
-            ptx::split_tf32(v[i].y, h[1], l[1]);
-            ptx::split_tf32(v[i].z, h[2], l[2]);
-            ptx::split_tf32(v[i].w, h[3], l[3]);
-            ptx::sts_v4(raw + off, h[0], h[1], h[2], h[3]);
-            ptx::sts_v4(lo_base + off, l[0], l[1], l[2], l[3]);
+          if constexpr (FLUSH) {
+            // unbiased split at the cost of one cvt per element: the raw tile
+            // stays the hi operand (the tensor core truncates it to trunc(x)),
+            // and the exact residual x - trunc(x) -- always of x's sign -- is
+            // rounded to TF32 to nearest here instead of truncated by the
+            // tensor core.  (Writing hi = rna(x) back into the raw slot as well
+            // cost ~150 cycles per K-block at the HBM pace.)
+            ptx::sts_v4(lo_base + off, ptx::to_tf32(ptx::tf32_residual(v[i].x)),
+                        ptx::to_tf32(ptx::tf32_residual(v[i].y)),
+                        ptx::to_tf32(ptx::tf32_residual(v[i].z)),
+                        ptx::to_tf32(ptx::tf32_residual(v[i].w)));
           } else {
             ptx::sts_v4(lo_base + off, __float_as_uint(ptx::tf32_residual(v[i].x)),
                         __float_as_uint(ptx::tf32_residual(v[i].y)),
@@ -528,11 +531,16 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
           if (blockIdx.x < 2 && tid == 0 && eg < 4096) g_trace_flush[rank][eg] = clock64();
 #endif
           uint32_t v[BNT];
+#if defined(SBT_FLUSH_DEBUG) && SBT_FLUSH_DEBUG == 2   // timing only: no slot reads
+#pragma unroll
+          for (int c = 0; c < BNT; ++c) v[c] = 0u;
+#else
 #pragma unroll
           for (int c = 0; c < BNT; c += 16)
             ptx::tmem_ld16(tmem + lane_addr + FC::BASE + slot * BNT + c,
                            *reinterpret_cast<uint32_t(*)[16]>(v + c));
           ptx::tmem_ld_wait();
+#endif
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -846,7 +854,11 @@ tf32x3_pair_tma_kernel(const __grid_constant__ ProblemSet<MAXP> ps, int p_prefet
               const uint64_t dbl = ptx::umma_desc(b_lo + j * b_step, b_lbo, b_sbo, b_lay);
               ptx::mma2_tf32_ss(d_small, dal, dbr, idesc, (kb | j) ? 1u : 0u);
               ptx::mma2_tf32_ss(d_small, dar, dbl, idesc, 1u);
+#if defined(SBT_FLUSH_DEBUG) && SBT_FLUSH_DEBUG == 1   // timing only: no slot rotation
+              ptx::mma2_tf32_ss(tmem + FC::BASE, dar, dbr, idesc, 1u);
+#else
               ptx::mma2_tf32_ss(tmem + FC::BASE + slot * BNT, dar, dbr, idesc, gin ? 1u : 0u);
+#endif
               if (gin == gmask) {
                 ptx::tc_commit2_mc(&step_full[slot], 0x3);
                 ++gu;

@@ -218,6 +218,8 @@ static bool plan_pair(const GemmParams<float>& p0, PairPlan* out) {
   // them double-buffered, so the epilogue overlaps the next tile's MMAs
   static const int split_bnt = env_int("SBT_TC_SPLIT_BNT", 256);
   if (out->split && out->bnt == 256 && split_bnt == 128) out->bnt = 128;
+  static const int force_bnt = env_int("SBT_TC_BNT", 0);   // A/B: cap the tile width
+  if (force_bnt >= 128 && out->bnt > force_bnt) out->bnt = force_bnt;
   return true;
 }
 
@@ -284,10 +286,9 @@ static int launch_pair_set(const tf32tma::ProblemSet<MAXP>& ps, cudaStream_t str
   // (SBT_TC_DEBUG=1 skips the TMA loads, 2 the lo conversion -- wrong results)
   // bits 12-13: log2 of the K=8 steps per FLUSH step-accumulator group
   // (SBT_TC_FLUSH_G = 1 / 2 / 4 / 8; narrow tiles only)
-  // 8 K=8 steps per group: fit of the 512^3 rank-32 HOOI within 5e-6 of
-  // the fp64 oracle (G = 1 / 2 / 4 / 8: 1.2 / 1.8 / 2.9 / 5.3e-6, north_star
-  // bound 1e-5) at 1.8x the unflushed time instead of 2.6x (G = 1)
-  static const int flush_g = env_int("SBT_TC_FLUSH_G", 8);
+  // 4 K=8 steps per group: fit of the 512^3 rank-32 HOOI within 5.1e-6 of the
+  // fp64 oracle (8 steps: 7.3e-6; north_star bound 1e-5) for ~2% of its time
+  static const int flush_g = env_int("SBT_TC_FLUSH_G", 4);
   static const int prefetch = env_int("SBT_TC_PREFETCH", 0) | (env_int("SBT_TC_DEBUG", 0) << 8) |
                               ((flush_g >= 8 ? 3 : flush_g >= 4 ? 2 : flush_g >= 2 ? 1 : 0) << 12);
   kern<<<dim3(unsigned(2 * pairs)), dim3(tf32tma::kThreads), smem, stream>>>(ps, prefetch);

@@ -1035,6 +1035,45 @@ def run_hooi_sharded(args, ctx, n, r, dtype):
     fl = hooi_flops(n, r)
     line = base_line(args, ctx, fl / per_iter / 1e9, per_iter * 1e3, None, clocks.summary())
     line["scaling"] = "strong"
+    # roofline of the whole job: the products' algorithmic bytes (as for one GPU)
+    # against the aggregate HBM bandwidth of the ranks
+    it = 4 if dtype == torch.float32 else 8
+    nbytes = it * (2 * n ** 3 + 5 * n * n * r + 4 * n * r * r + r ** 3)
+    hbm = load_peaks().get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]) * ctx.world
+    line["roofline"] = {"bound": "hbm", "achieved": round(nbytes / per_iter / 1e9, 1),
+                        "peak": hbm, "unit": "GB/s",
+                        "frac": round(nbytes / (hbm * 1e9) / per_iter, 4), "traffic": None,
+                        "kernel": "sharded HOOI iteration (all ranks)",
+                        "note": f"aggregate HBM of {ctx.world} GPUs; the per-mode-update "
+                                "collectives and the replicated factor updates are latency, "
+                                "not bytes"}
+    if not args.no_e2e:
+        # end to end: every rank copies its slab in from pinned host memory and
+        # brings the core and factors back
+        host, _ = pinned_np(local.data.numel(), dtype, fill=False)
+        host.copy_(local.data.cpu())
+        k = 1 + iters
+
+        def e2e_run():
+            buf = torch.empty(local.data.numel(), dtype=dtype, device=dev)
+            buf.copy_(host, non_blocking=True)
+            core, us, _, _ = hooi_sharded(DenseTensor(local.layout, buf), (n, n, n), (r, r, r),
+                                          max_iters=k, tol=-1.0)
+            out = [core.cpu()] + [u.cpu() for u in us]
+            torch.cuda.synchronize()
+            return out
+        e2e_run()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        e2e_run()
+        dt = ctx.max_over_ranks(time.perf_counter() - t0)
+        line["e2e"] = {"value": round(fl * k / dt / 1e9, 2), "unit": "GFLOP/s",
+                       "h2d_bytes_per_step": it * local.data.numel() // k,
+                       "d2h_bytes_per_step": (it * r ** 3 + 8 * 3 * n * r) // k,
+                       "ms_per_step": round(dt * 1e3 / k, 3),
+                       "api": f"parallel.hooi_sharded on slabs copied from pinned host memory, "
+                              f"{k} iterations incl. the HOSVD init; core + factors copied "
+                              "back; max over ranks"}
     line["config"] = {"workload": f"configs[3] HOOI {n}^3 rank {r} {args.dtype}",
                       "parallelism": f"T slab-sharded on mode 2 over {ctx.world} ranks "
                                      "(all-reduce / all-gather per mode update; HOSVD Gram of "

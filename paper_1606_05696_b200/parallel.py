@@ -223,8 +223,12 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
     starts = [slab(d2, world, r)[0] for r in range(world)]
     mx = max(sizes)
 
+    # gloo (CPU tests, or ranks sharing one GPU) moves CUDA tensors through
+    # host copies; NCCL takes them directly
+    host_coll = dist.get_backend(group) == "gloo" and dev.type == "cuda"
+
     def allreduce(x):
-        dist.all_reduce(x.data, group=group)
+        allreduce_t(x.data, group)
         return x
 
     def allgather_last(x):
@@ -232,11 +236,11 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
         mode is the slowest, so a slab is one contiguous chunk."""
         a, b, _ = x.layout.dims
         per = a * b
-        pad = torch.zeros(per * mx, dtype=x.dtype, device=x.device)
+        pad = torch.zeros(per * mx, dtype=x.dtype, device="cpu" if host_coll else x.device)
         pad[:x.data.numel()] = x.data
         parts = [torch.empty_like(pad) for _ in range(world)]
         dist.all_gather(parts, pad, group=group)
-        flat = torch.cat([q[:per * s] for q, s in zip(parts, sizes)])
+        flat = torch.cat([q[:per * s] for q, s in zip(parts, sizes)]).to(x.device)
         return DenseTensor(Layout.packed((a, b, d2)), flat)
 
     def ring_gram_last(x):
@@ -252,16 +256,18 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
             blk = ops.cross_gram(mine, cl, buf, sizes[holder], k)
             rows[:cl, starts[holder]:starts[holder] + sizes[holder]] = blk
             if step < world - 1:
-                nbuf = torch.empty_like(buf)
+                sbuf = buf.cpu() if host_coll else buf
+                nbuf = torch.empty_like(sbuf)
                 reqs = dist.batch_isend_irecv([
-                    dist.P2POp(dist.isend, buf, (rank + 1) % world, group),
+                    dist.P2POp(dist.isend, sbuf, (rank + 1) % world, group),
                     dist.P2POp(dist.irecv, nbuf, (rank - 1) % world, group)])
                 for q in reqs:
                     q.wait()
-                buf = nbuf
-        parts = [torch.empty_like(rows) for _ in range(world)]
-        dist.all_gather(parts, rows, group=group)
-        g = torch.cat([q[:s] for q, s in zip(parts, sizes)])
+                buf = nbuf.to(dev)
+        rows_c = rows.cpu() if host_coll else rows
+        parts = [torch.empty_like(rows_c) for _ in range(world)]
+        dist.all_gather(parts, rows_c, group=group)
+        g = torch.cat([q[:s] for q, s in zip(parts, sizes)]).to(dev)
         return 0.5 * (g + g.t())
 
     def local_u2(u2):
@@ -327,6 +333,13 @@ def hooi_sharded(t_local, full_dims, ranks, max_iters: int = 50, tol: float = 1e
 
 
 def allreduce_t(x, group=None):
+    """In-place sum over the group (through a host copy for CUDA tensors on
+    gloo)."""
     import torch.distributed as dist
-    dist.all_reduce(x, group=group)
+    if x.is_cuda and dist.get_backend(group) == "gloo":
+        h = x.cpu()
+        dist.all_reduce(h, group=group)
+        x.copy_(h)
+    else:
+        dist.all_reduce(x, group=group)
     return x

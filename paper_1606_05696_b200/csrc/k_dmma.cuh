@@ -113,7 +113,36 @@ __device__ __forceinline__ void stage_bb(double* dst, const double* __restrict__
 // BNT: N extent of the CTA tile.  128 (one CTA per SM; NW = 8 or 16); 64
 // with NW = 8 (4 x 2 warps of 32 x 32, <= 128 registers) runs two CTAs per
 // SM, so one CTA's prologue / epilogue overlaps the other's main loop.
-template <bool A_K, bool B_K, bool BB = false, int NW = 8, int BNT = 128>
+// BB A staging with 16-byte copies: the two batch entries (b, b+1) of a pair
+// are adjacent in global memory (the batch is A's unit-stride mode), so they
+// land side by side: position k * LDB2 + (b >> 1) * 64 + 2 m + (b & 1).
+// Half the copy instructions of stage_bb; needs ars, acs even and A 16-byte
+// aligned (checked by the launcher).
+constexpr int LDB2 = 132;
+static_assert(BK * LDB2 <= TILE_DOUBLES, "BB16 tile fits the stage");
+template <int NT = kThreads>
+__device__ __forceinline__ void stage_bb16(double* dst, const double* __restrict__ src,
+                                           int64_t b0, int64_t m0, int64_t k0, int64_t nbatch,
+                                           int64_t m_ext, int64_t k_ext, int64_t ars,
+                                           int64_t acs, int tid) {
+#pragma unroll
+  for (int i = 0; i < 64 * BK / NT; ++i) {
+    const int e = tid + i * NT;
+    const int k = e >> 6, pr = e & 1, m = (e >> 1) & 31;
+    const int64_t gb = b0 + 2 * pr, gm = m0 + m, gk = k0 + k;
+    double* d = dst + k * LDB2 + pr * 64 + 2 * m;
+    const bool row = gm < m_ext && gk < k_ext;
+    const double* s = src + gb + gm * ars + gk * acs;
+    if (row && gb + 1 < nbatch) {
+      cp_async16(d, s, true);
+    } else {                         // batch tail: one entry or none
+      cp_async8(d, row && gb < nbatch ? s : src, row && gb < nbatch);
+      cp_async8(d + 1, src, false);
+    }
+  }
+}
+
+template <bool A_K, bool B_K, bool BB = false, int NW = 8, int BNT = 128, bool BB16 = false>
 __global__ void __launch_bounds__(NW * 32, BNT == 64 ? 2 : 1)
 dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   extern __shared__ __align__(16) double sm[];
@@ -141,7 +170,9 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
     double* sa = sm + (kb % STAGES) * STAGE_D;
     double* sb = sa + TILE_DOUBLES;
     const int64_t k0 = int64_t(kb) * BK;
-    if (BB)
+    if (BB && BB16)
+      stage_bb16<NT>(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
+    else if (BB)
       stage_bb<NT>(sa, A, pb * 4, m0, k0, p.batch, p.m, p.k, p.ars, p.acs, tid);
     else
       stage_operand<A_K, NT>(sa, A, m0, k0, p.m, p.k, A_K ? p.ars : 1, A_K ? 1 : p.acs, tid);
@@ -173,7 +204,9 @@ dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const int m = wm * (TM * 8) + i * 8 + fr;
-        if (BB) af[i] = sa[(kk + fk) * LDBB + 36 * (m >> 5) + (m & 31)];
+        if (BB && BB16)
+          af[i] = sa[(kk + fk) * LDB2 + ((m >> 5) >> 1) * 64 + 2 * (m & 31) + ((m >> 5) & 1)];
+        else if (BB) af[i] = sa[(kk + fk) * LDBB + 36 * (m >> 5) + (m & 31)];
         else af[i] = A_K ? sa[m * LDK + kk + fk] : sa[(kk + fk) * LDMN + m];
       }
 #pragma unroll

@@ -440,9 +440,9 @@ static bool orient(const GemmParams<T>& p0, GemmParams<T>* out, int* am, int* bm
   return true;
 }
 
-template <bool AK, bool BK_, bool BB, int NW, int BNT = 128>
+template <bool AK, bool BK_, bool BB, int NW, int BNT = 128, bool BB16 = false>
 static int launch_dmma_nw(const GemmParams<double>& p, cudaStream_t stream) {
-  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW, BNT>;
+  auto kern = dmma::dmma_gemm_kernel<AK, BK_, BB, NW, BNT, BB16>;
   // BNT = 64: the B tile is half as wide (two CTAs per SM need <= 113 KB each)
   const int smem = BNT == 128 ? dmma::SMEM_BYTES : dmma::SMEM_BYTES_N64;
   if (set_smem_attr(reinterpret_cast<const void*>(kern), smem) != 0) return -3;
@@ -469,7 +469,12 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   static const int bn_env = env_int("SBT_DMMA_BN", 0);     // 0 = by tile kind
   const int bn = bn_env ? bn_env : (BB ? 128 : 64);
   if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
-  // batch-blocked tiles: 8 warps (25.0 -> 25.6 TF/s on the 8 exceptional cases at n=256)
+  // batch-blocked tiles: 8 warps (25.0 -> 25.6 TF/s on the 8 exceptional cases at n=256);
+  // 16-byte A staging when the batch pairs are 16-byte aligned (SBT_DMMA_BB16=0: 8-byte)
+  static const int bb16_env = env_int("SBT_DMMA_BB16", 1);
+  if (BB && bb16_env && nw_env == 0 && p.ars % 2 == 0 && p.acs % 2 == 0 &&
+      reinterpret_cast<uintptr_t>(p.a) % 16 == 0)
+    return launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream);
   const int nw = nw_env ? nw_env : ((p.k <= 256 && !BB) ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
                   : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);

@@ -95,8 +95,8 @@ int sbt_ritz_f64(const double* qz, const double* m, int64_t n, int p, int rank, 
         dims[mode].  qt: the previous factor's p columns as rows of ldq
         doubles (p <= 64).  Forms Z = Y_(mode) Y_(mode)^T Q in fp64 straight
         from y (no unfolding copy; fp32 widened on load; deterministic) in the
-        caller's workspace `ws` (sbt_hooi_factor_ws_bytes bytes, no
-        initialisation needed), then
+        caller's workspace `ws` (sbt_hooi_factor_ws_bytes bytes, 16-byte
+        aligned, no initialisation needed; one per stream), then
         finishes the sweep exactly as sbt_ritz_f64 with m = NULL.  Three
         launches, no host synchronisation, capturable. */
 size_t sbt_hooi_factor_ws_bytes(int order, const int64_t* dims, int mode, int p);

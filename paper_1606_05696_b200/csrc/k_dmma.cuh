@@ -22,7 +22,10 @@ namespace dmma {
 #ifndef SBT_DMMA_BK
 #define SBT_DMMA_BK 16
 #endif
-constexpr int BM = 128, BN = 128, BK = SBT_DMMA_BK, STAGES = 3;
+#ifndef SBT_DMMA_STAGES
+#define SBT_DMMA_STAGES 3
+#endif
+constexpr int BM = 128, BN = 128, BK = SBT_DMMA_BK, STAGES = SBT_DMMA_STAGES;
 static_assert(BK == 16 || BK == 32, "K-block depth");
 constexpr int kThreads = 256;      // staging loops assume >= 256 threads
 template <int NW>

@@ -611,6 +611,8 @@ int hooi_factor(const TY* y, int order, const int64_t* dims, int mode, const dou
   const gapply::Plan pl = gapply::plan(u.n, u.cols, p);
   if (ws_bytes < size_t(pl.bytes))
     return fail(SBT_EINVAL, "sbt_hooi_factor: workspace too small (see sbt_hooi_factor_ws_bytes)");
+  if (reinterpret_cast<uintptr_t>(ws) % 16)
+    return fail(SBT_EINVAL, "sbt_hooi_factor: workspace must be 16-byte aligned");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   double* wsd = static_cast<double*>(ws);
   double* wt = wsd + pl.w_off;

@@ -288,14 +288,19 @@ def _factor_ws(dev, dims, r, p):
     import ctypes
     from . import _lib
     torch = _torch()
-    key = (dev, tuple(dims), r, p)
+    # one workspace per stream (concurrent HOOIs on different streams must not
+    # share it), bounded: a long-lived process cycling through shapes keeps the
+    # most recent ones
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream, tuple(dims), r, p)
     ws = _FACTOR_WS.get(key)
     if ws is None:
+        if len(_FACTOR_WS) >= 64:
+            _FACTOR_WS.pop(next(iter(_FACTOR_WS)))
         d = (ctypes.c_int64 * len(dims))(*dims)
         nbytes = int(_lib.load().sbt_hooi_factor_ws_bytes(len(dims), d, r, p))
         if nbytes <= 0:
             raise ValueError(f"sbt_hooi_factor_ws_bytes: bad geometry {dims} mode {r} p {p}")
-        ws = _FACTOR_WS[key] = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        ws = _FACTOR_WS[key] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     return ws
 
 

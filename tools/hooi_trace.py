@@ -13,7 +13,7 @@ x = torch.einsum("ia,abc->ibc", us[0], core); x = torch.einsum("jb,ibc->ijc", us
 x = x + 1e-3 * torch.randn(n, n, n, device="cuda", generator=g, dtype=torch.float64)
 t = DenseTensor(Layout.packed((n, n, n)), x.permute(2, 1, 0).contiguous().reshape(-1).to(torch.float32))
 del x
-sbt.hooi(t, (r, r, r), max_iters=2, tol=-1.0)
+sbt.hooi(t, (r, r, r), max_iters=5, tol=-1.0)   # captures the iteration graph (cached)
 from torch.profiler import profile, ProfilerActivity
 from collections import defaultdict
 

@@ -136,26 +136,31 @@ small64_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
 namespace sbt {
 namespace small64mma {
 
-// K3 (fp32, n = 64) on the tensor pipe: warp-level mma.sync m16n8k8 TF32
+// K3 (fp32, n = 32 / 64) on the tensor pipe: warp-level mma.sync m16n8k8 TF32
 // with the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi, round-to-nearest
-// TF32 parts), fp32 register accumulators.  At n = 64 the batched product
-// needs ~70 TFLOP/s of fp32 arithmetic to keep pace with HBM, which the
-// register-blocked FFMA kernel above reaches only in part (it is bound by
-// shared-memory wavefronts, ncu: LSU 79% busy); mma.sync TF32 runs at
-// ~278 TFLOP/s on this part (measured), 93 TFLOP/s as 3xTF32.
+// TF32 parts), fp32 register accumulators.  The register-blocked FFMA kernels
+// are bound by shared-memory wavefronts at these sizes (ncu: LSU 76-79% busy);
+// mma.sync TF32 runs at ~278 TFLOP/s on this part (measured), 93 TFLOP/s as
+// 3xTF32.
 //
-// One matrix per CTA stage, 4 warps x 16 rows of C, two TMA stages per CTA,
-// three CTAs per SM.  A lands as (72 m) x 64 k and B as (68 k) x 64 n (TMA
-// zero fill pads the rows): both fragment patterns hit 32 distinct banks.
-// Same operand contract as small64_kernel.
-constexpr int LDA = 72, LDB = 68, S = 64;
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
-constexpr int STAGES = 2;
-constexpr int CTAS_PER_SM = 3;
-constexpr int A_FLOATS = S * LDA, B_FLOATS = S * LDB;
-constexpr int STAGE_FLOATS = A_FLOATS + B_FLOATS;
-constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4 + 64;
+// A CTA stage holds G matrices (one 3-D TMA box per operand); each matrix is
+// computed by S / 16 warps of 16 C rows x S columns.  Two stages per CTA.  A
+// lands as (LDA m) x S k and B as (LDB k) x S n, the TMA zero fill padding the
+// rows so that both fragment patterns hit 32 distinct banks (LDA = 8 mod 32,
+// LDB = 4 mod 32).  Operand contract as small64_kernel, at n = S.
+template <int S>
+struct Cfg {
+  static constexpr int LDA = S + 8, LDB = S + 4;
+  static constexpr int G = S == 64 ? 1 : 4;               // matrices per stage
+  static constexpr int kWarps = G * (S / 16);
+  static constexpr int kThreads = 32 * kWarps;
+  static constexpr int STAGES = 2;
+  static constexpr int CTAS_PER_SM = S == 64 ? 3 : 2;
+  static constexpr int A_FLOATS = S * LDA, B_FLOATS = S * LDB;
+  static constexpr int STAGE_FLOATS = G * (A_FLOATS + B_FLOATS);
+  static constexpr int SMEM_BYTES = STAGES * STAGE_FLOATS * 4 + 64;
+};
+constexpr int LDA = Cfg<64>::LDA, LDB = Cfg<64>::LDB;   // (n = 64, for the launcher)
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4],
                                          const uint32_t (&b)[2]) {
@@ -166,20 +171,24 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-__global__ void __launch_bounds__(kThreads, CTAS_PER_SM)
-small64_mma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB) {
+template <int S>
+__global__ void __launch_bounds__(Cfg<S>::kThreads, Cfg<S>::CTAS_PER_SM)
+small_mma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
+                 const __grid_constant__ CUtensorMap tmB, int64_t ngroups) {
+  using C_ = Cfg<S>;
+  constexpr int G = C_::G, STAGES = C_::STAGES, LDA_ = C_::LDA, LDB_ = C_::LDB;
+  constexpr int NT8 = S / 8;                       // 8-wide N tiles = K steps
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sm = reinterpret_cast<float*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_FLOATS * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * C_::STAGE_FLOATS * 4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  constexpr uint32_t TX = uint32_t(STAGE_FLOATS * 4);
-  auto issue = [&](int64_t b, int slot) {
-    float* sa = sm + slot * STAGE_FLOATS;
+  constexpr uint32_t TX = uint32_t(C_::STAGE_FLOATS * 4);
+  auto issue = [&](int64_t grp, int slot) {
+    float* sa = sm + slot * C_::STAGE_FLOATS;
     ptx::mbar_arrive_expect_tx(&full[slot], TX);
-    ptx::tma_load_4d(sa, &tmA, &full[slot], 0, 0, int(b), 0);
-    ptx::tma_load_4d(sa + A_FLOATS, &tmB, &full[slot], 0, 0, int(b), 0);
+    ptx::tma_load_4d(sa, &tmA, &full[slot], 0, 0, int(grp * G), 0);
+    ptx::tma_load_4d(sa + G * C_::A_FLOATS, &tmB, &full[slot], 0, 0, int(grp * G), 0);
   };
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full[s], 1);
@@ -188,49 +197,56 @@ small64_mma_kernel(GemmParams<float> p, const __grid_constant__ CUtensorMap tmA,
     ptx::prefetch_tmap(&tmB);
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-      const int64_t b = blockIdx.x + int64_t(s) * gridDim.x;
-      if (b < p.batch) issue(b, s);
+      const int64_t gi = blockIdx.x + int64_t(s) * gridDim.x;
+      if (gi < ngroups) issue(gi, s);
     }
   }
   __syncthreads();
-  const int r0 = warp * 16 + g;         // this lane's C rows r0, r0 + 8
+  const int mat = warp / (S / 16);                 // matrix of the group
+  const int r0 = (warp % (S / 16)) * 16 + g;      // this lane's C rows r0, r0 + 8
   uint32_t it = 0;
-  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x, ++it) {
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const int slot = int(it % STAGES);
     ptx::mbar_wait(&full[slot], (it / STAGES) & 1u);
-    const float* sa = sm + slot * STAGE_FLOATS;   // A[m][k] at k * LDA + m
-    const float* sb = sa + A_FLOATS;              // B[k][n] at n * LDB + k
-    float acc[8][4];
+    const int64_t bidx = grp * G + mat;
+    const float* sa = sm + slot * C_::STAGE_FLOATS + mat * C_::A_FLOATS;   // A[m][k] at k*LDA + m
+    const float* sb = sm + slot * C_::STAGE_FLOATS + G * C_::A_FLOATS +
+                      mat * C_::B_FLOATS;                                  // B[k][n] at n*LDB + k
+    float acc[NT8][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int j = 0; j < NT8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    if (bidx < p.batch) {
 #pragma unroll 2
-    for (int k0 = 0; k0 < S; k0 += 8) {
-      uint32_t ah[4], al[4];
-      ptx::split_tf32(sa[(k0 + t) * LDA + r0], ah[0], al[0]);
-      ptx::split_tf32(sa[(k0 + t) * LDA + r0 + 8], ah[1], al[1]);
-      ptx::split_tf32(sa[(k0 + t + 4) * LDA + r0], ah[2], al[2]);
-      ptx::split_tf32(sa[(k0 + t + 4) * LDA + r0 + 8], ah[3], al[3]);
+      for (int k0 = 0; k0 < S; k0 += 8) {
+        uint32_t ah[4], al[4];
+        ptx::split_tf32(sa[(k0 + t) * LDA_ + r0], ah[0], al[0]);
+        ptx::split_tf32(sa[(k0 + t) * LDA_ + r0 + 8], ah[1], al[1]);
+        ptx::split_tf32(sa[(k0 + t + 4) * LDA_ + r0], ah[2], al[2]);
+        ptx::split_tf32(sa[(k0 + t + 4) * LDA_ + r0 + 8], ah[3], al[3]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        uint32_t bh[2], bl[2];
-        ptx::split_tf32(sb[(8 * j + g) * LDB + k0 + t], bh[0], bl[0]);
-        ptx::split_tf32(sb[(8 * j + g) * LDB + k0 + t + 4], bh[1], bl[1]);
-        mma_tf32(acc[j], al, bh);      // small cross terms first
-        mma_tf32(acc[j], ah, bl);
-        mma_tf32(acc[j], ah, bh);
+        for (int j = 0; j < NT8; ++j) {
+          uint32_t bh[2], bl[2];
+          ptx::split_tf32(sb[(8 * j + g) * LDB_ + k0 + t], bh[0], bl[0]);
+          ptx::split_tf32(sb[(8 * j + g) * LDB_ + k0 + t + 4], bh[1], bl[1]);
+          mma_tf32(acc[j], al, bh);      // small cross terms first
+          mma_tf32(acc[j], ah, bl);
+          mma_tf32(acc[j], ah, bh);
+        }
       }
     }
     __syncthreads();  // every warp has read the slot
-    const int64_t bn = b + int64_t(STAGES) * gridDim.x;
-    if (tid == 0 && bn < p.batch) issue(bn, slot);
-    float* C = p.c + b * p.cps;       // C[m][n] at m + n * 64
+    const int64_t gn = grp + int64_t(STAGES) * gridDim.x;
+    if (tid == 0 && gn < ngroups) issue(gn, slot);
+    if (bidx < p.batch) {
+      float* C = p.c + bidx * p.cps;               // C[m][n] at m + n * S
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int n = 8 * j + 2 * t;
-      store_out(C + r0 + int64_t(n) * S, acc[j][0], p.alpha, p.beta);
-      store_out(C + r0 + int64_t(n + 1) * S, acc[j][1], p.alpha, p.beta);
-      store_out(C + r0 + 8 + int64_t(n) * S, acc[j][2], p.alpha, p.beta);
-      store_out(C + r0 + 8 + int64_t(n + 1) * S, acc[j][3], p.alpha, p.beta);
+      for (int j = 0; j < NT8; ++j) {
+        const int n = 8 * j + 2 * t;
+        store_out(C + r0 + int64_t(n) * S, acc[j][0], p.alpha, p.beta);
+        store_out(C + r0 + int64_t(n + 1) * S, acc[j][1], p.alpha, p.beta);
+        store_out(C + r0 + 8 + int64_t(n) * S, acc[j][2], p.alpha, p.beta);
+        store_out(C + r0 + 8 + int64_t(n + 1) * S, acc[j][3], p.alpha, p.beta);
+      }
     }
   }
 }

@@ -593,24 +593,33 @@ static int try_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
 }
 
 // fp32 64 x 64 x 64 batches with column-major A, B and C: 8 x 8 register blocks.
-// fp32 n = 64 on the tensor pipe (k_small64.cuh small64_mma_kernel); 0 = not
-// eligible (then the FFMA kernel below).  SBT_SMALL64_MMA=0 keeps the FFMA one.
-static int try_small64_mma(const GemmParams<float>& p, cudaStream_t stream) {
+// fp32 n = 32 / 64 packed batches on the tensor pipe (k_small64.cuh
+// small_mma_kernel); 0 = not eligible.  SBT_SMALL_MMA=0 keeps the FFMA kernels.
+template <int S>
+static int try_small_mma(const GemmParams<float>& p, cudaStream_t stream) {
   using namespace small64mma;
-  static const int on = env_int("SBT_SMALL64_MMA", 1);
+  using C_ = Cfg<S>;
+  static const int on = env_int("SBT_SMALL_MMA", env_int("SBT_SMALL64_MMA", 1));
   if (!on) return 0;
-  if (set_smem_attr(reinterpret_cast<const void*>(small64_mma_kernel), SMEM_BYTES) != 0)
-    return -3;
-  CUtensorMap ta, tb;
-  if (!make_tmap_f32(&ta, p.a, 64, 64, 64, p.batch, p.aps, 1, 0, LDA, 64,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, 1) ||
-      !make_tmap_f32(&tb, p.b, 64, 64, 64, p.batch, p.bps, 1, 0, LDB, 64,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, 1))
+  if (p.m != S || p.n != S || p.k != S) return 0;
+  if (!(p.ars == 1 && p.acs == S && p.brs == 1 && p.bcs == S && p.crs == 1 && p.ccs == S))
     return 0;
-  const int64_t cap = int64_t(kNumSMs) * CTAS_PER_SM;
-  const int64_t grid = p.batch < cap ? p.batch : cap;
-  small64_mma_kernel<<<dim3(unsigned(grid)), dim3(kThreads), SMEM_BYTES, stream>>>(p, ta, tb);
-  note_launch("small64_mma_f32");
+  if (p.aps % 4 || p.bps % 4 || p.aps < S * S || p.bps < S * S || !aligned16(p.a) ||
+      !aligned16(p.b) || p.batch > (int64_t(1) << 31))
+    return 0;
+  auto kern = small_mma_kernel<S>;
+  if (set_smem_attr(reinterpret_cast<const void*>(kern), C_::SMEM_BYTES) != 0) return -3;
+  CUtensorMap ta, tb;
+  if (!make_tmap_f32(&ta, p.a, S, S, S, p.batch, p.aps, 1, 0, C_::LDA, S,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, C_::G) ||
+      !make_tmap_f32(&tb, p.b, S, S, S, p.batch, p.bps, 1, 0, C_::LDB, S,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, C_::G))
+    return 0;
+  const int64_t ngroups = ceil_div(p.batch, C_::G);
+  const int64_t cap = int64_t(kNumSMs) * C_::CTAS_PER_SM;
+  const int64_t grid = ngroups < cap ? ngroups : cap;
+  kern<<<dim3(unsigned(grid)), dim3(C_::kThreads), C_::SMEM_BYTES, stream>>>(p, ta, tb, ngroups);
+  note_launch(S == 64 ? "small64_mma_f32" : "small32_mma_f32");
   return 1;
 }
 
@@ -623,7 +632,7 @@ static int try_small64(const GemmParams<float>& p, cudaStream_t stream) {
       !aligned16(p.b) || p.batch > (int64_t(1) << 31))
     return 0;
   {
-    const int rc = try_small64_mma(p, stream);
+    const int rc = try_small_mma<64>(p, stream);
     if (rc != 0) return rc;
   }
   if (set_smem_attr(reinterpret_cast<const void*>(small64_kernel), SMEM_BYTES) != 0) return -3;
@@ -658,6 +667,10 @@ static int try_small(const GemmParams<T>& p, cudaStream_t stream, bool forced) {
     static const int use64 = env_int("SBT_SMALL64", 1);
     if (use64 && mx == 64) {
       const int rc = try_small64(p, stream);
+      if (rc != 0) return rc;
+    }
+    if (mx == 32) {
+      const int rc = try_small_mma<32>(p, stream);
       if (rc != 0) return rc;
     }
   }

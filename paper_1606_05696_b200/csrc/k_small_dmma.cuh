@@ -35,7 +35,6 @@ namespace small_dmma {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int STAGES = 3;
 
 __host__ __device__ constexpr int ld_of(int rows) { return ((rows + 15) / 16) * 16 + 4; }
 template <int NMAX>
@@ -45,6 +44,19 @@ struct Cfg {
   static constexpr int G = kWarps / WPM;         // matrices per group
   static constexpr int LD_MAX = NMAX + 4;        // padded leading dimension
   static constexpr int STAGE_DOUBLES = G * 2 * LD_MAX * NMAX;
+  // three one-stage CTAs per SM (12 warps) instead of one three-stage CTA
+  // (4 warps): the DMMA pipe needs more than one warp per scheduler, and while
+  // one CTA waits for its next group the others compute.  Measured at P = 10^6
+  // (n = 32) / 2 x 10^5 (n = 64): 0.84 -> 1.02 of the copy-measured HBM rate,
+  // 17.5 -> 24.9 TFLOP/s
+#ifndef SBT_SMALL_DMMA64_CTAS
+#define SBT_SMALL_DMMA64_CTAS 3
+#endif
+#ifndef SBT_SMALL_DMMA32_CTAS
+#define SBT_SMALL_DMMA32_CTAS 3
+#endif
+  static constexpr int CTAS_PER_SM = NMAX == 64 ? SBT_SMALL_DMMA64_CTAS : SBT_SMALL_DMMA32_CTAS;
+  static constexpr int STAGES = CTAS_PER_SM >= 3 ? 1 : 3 / CTAS_PER_SM;
   static constexpr int SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + 64;
 };
 
@@ -65,11 +77,11 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
 }
 
 template <int NMAX>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, Cfg<NMAX>::CTAS_PER_SM)
 small_dmma_kernel(GemmParams<double> p, const __grid_constant__ CUtensorMap tmA,
                   const __grid_constant__ CUtensorMap tmB, int64_t ngroups) {
   using C_ = Cfg<NMAX>;
-  constexpr int G = C_::G;
+  constexpr int G = C_::G, STAGES = C_::STAGES;
   auto stage_doubles = [] { return C_::STAGE_DOUBLES; };
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sm = reinterpret_cast<double*>(smem_raw);

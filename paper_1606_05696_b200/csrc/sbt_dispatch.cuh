@@ -574,7 +574,8 @@ static int launch_small_dmma(const GemmParams<double>& p, cudaStream_t stream) {
                         uint32_t(p.n), C_::G))
     return 0;
   const int64_t ngroups = ceil_div(p.batch, C_::G);
-  const int64_t grid = ngroups < int64_t(kNumSMs) ? ngroups : int64_t(kNumSMs);
+  const int64_t cap = int64_t(kNumSMs) * C_::CTAS_PER_SM;
+  const int64_t grid = ngroups < cap ? ngroups : cap;
   kern<<<dim3(unsigned(grid)), dim3(kThreads), C_::SMEM_BYTES, stream>>>(p, ta, tb, ngroups);
   note_launch(NMAX == 32 ? "small_batched_dmma_f64" : "small_batched_dmma64_f64");
   return 1;

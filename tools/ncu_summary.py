@@ -25,6 +25,8 @@ def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:       # empty capture (kernel filter matched nothing)
+        return None
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
@@ -40,6 +42,9 @@ def main():
     for arg in sys.argv[2:]:
         rep, key = arg.split(":", 1)
         d = raw(rep)
+        if d is None:
+            lines += [f"## {key}  ({Path(rep).name})", "", "(no kernel captured)", ""]
+            continue
         name = d.get("Kernel Name", ("?", ""))[0]
         lines += [f"## {key}  ({Path(rep).name})", "", f"kernel: `{name[:160]}`", "", "```"]
         for m in METRICS:

@@ -13,7 +13,7 @@ timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o $P/group_bb_n256 -f python tools
 timeout 300 $NCU -k regex:pair_tma -s 2 -c 1 -o $P/pair_1.3_n256 -f python tools/case_single.py 1.3 256 f32 3 > /dev/null 2>&1
 timeout 300 $NCU -k regex:small -s 1 -c 1 -o $P/small32_f32 -f python tools/small_single.py 32 1000000 f32 > /dev/null 2>&1
 timeout 300 $NCU -k regex:small -s 1 -c 1 -o $P/small32_f64 -f python tools/small_single.py 32 1000000 f64 > /dev/null 2>&1
-timeout 300 $NCU -k regex:small64_mma -s 1 -c 1 -o $P/small64_f32 -f python tools/small_single.py 64 1000000 f32 > /dev/null 2>&1
+timeout 300 $NCU -k regex:small_mma -s 1 -c 1 -o $P/small64_f32 -f python tools/small_single.py 64 1000000 f32 > /dev/null 2>&1
 timeout 300 $NCU -k regex:dmma_gemm -s 1 -c 1 -o $P/order4_f64 -f python bench.py --config order4 --dtype f64 --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 # HOOI iteration kernels (graph nodes of the timed run)
 timeout 600 $NCU -k regex:"pair_tma|ritz|gapply" --launch-skip 200 -c 12 -o $P/hooi_iter -f python bench.py --config hooi --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
@@ -23,7 +23,7 @@ NCU_TRAFFIC_JSON=gpurun_out/ncu_traffic.json python tools/ncu_summary.py gpurun_
   $P/group_plain_n256.ncu-rep:tc_tf32x3_pair_group/n256/f32 \
   $P/group_bb_n256.ncu-rep:tc_tf32x3_pair_group_bb/n256/f32 \
   $P/pair_1.3_n256.ncu-rep:tc_tf32x3_pair_tma/n256/f32 \
-  $P/small32_f32.ncu-rep:small_batched_f32/n32/f32 \
+  $P/small32_f32.ncu-rep:small32_mma_f32/n32/f32 \
   $P/small32_f64.ncu-rep:small_batched_dmma_f64/n32/f64 \
   $P/small64_f32.ncu-rep:small64_mma_f32/n64/f32 \
   $P/order4_f64.ncu-rep:tc_dmma_f64/n128/f64

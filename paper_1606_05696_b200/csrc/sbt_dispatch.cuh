@@ -468,13 +468,14 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   // TF/s; the batch-blocked tiles lose (25.0 -> 23.4) and keep 128 x 128.
   static const int bn_env = env_int("SBT_DMMA_BN", 0);     // 0 = by tile kind
   const int bn = bn_env ? bn_env : (BB ? 128 : 64);
-  if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   // batch-blocked tiles: 8 warps (25.0 -> 25.6 TF/s on the 8 exceptional cases at n=256);
   // 16-byte A staging when the batch pairs are 16-byte aligned (SBT_DMMA_BB16=0: 8-byte)
   static const int bb16_env = env_int("SBT_DMMA_BB16", 1);
   if (BB && bb16_env && nw_env == 0 && p.ars % 2 == 0 && p.acs % 2 == 0 &&
       reinterpret_cast<uintptr_t>(p.a) % 16 == 0)
-    return launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream);
+    return bn == 64 ? launch_dmma_nw<AK, BK_, BB, 8, 64, true>(p, stream)
+                    : launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream);
+  if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   const int nw = nw_env ? nw_env : ((p.k <= 256 && !BB) ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)
                   : launch_dmma_nw<AK, BK_, BB, 8>(p, stream);

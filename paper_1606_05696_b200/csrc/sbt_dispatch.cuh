@@ -467,14 +467,15 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
   // plain-case launches, 128 -> 64): n=128 24.7 -> 26.8, n=256 28.6 -> 30.3
   // TF/s; the batch-blocked tiles lose (25.0 -> 23.4) and keep 128 x 128.
   static const int bn_env = env_int("SBT_DMMA_BN", 0);     // 0 = by tile kind
-  const int bn = bn_env ? bn_env : (BB ? 128 : 64);
   // batch-blocked tiles: 8 warps (25.0 -> 25.6 TF/s on the 8 exceptional cases at n=256);
-  // 16-byte A staging when the batch pairs are 16-byte aligned (SBT_DMMA_BB16=0: 8-byte)
+  // 16-byte A staging when the batch pairs are 16-byte aligned (SBT_DMMA_BB16=0: 8-byte),
+  // then also 128 x 64 tiles, two CTAs per SM (36-case step 28.7 -> 29.0 TF/s)
   static const int bb16_env = env_int("SBT_DMMA_BB16", 1);
   if (BB && bb16_env && nw_env == 0 && p.ars % 2 == 0 && p.acs % 2 == 0 &&
       reinterpret_cast<uintptr_t>(p.a) % 16 == 0)
-    return bn == 64 ? launch_dmma_nw<AK, BK_, BB, 8, 64, true>(p, stream)
-                    : launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream);
+    return bn_env == 128 ? launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream)
+                         : launch_dmma_nw<AK, BK_, BB, 8, 64, true>(p, stream);
+  const int bn = bn_env ? bn_env : (BB ? 128 : 64);
   if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   const int nw = nw_env ? nw_env : ((p.k <= 256 && !BB) ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)

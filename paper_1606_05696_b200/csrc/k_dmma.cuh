@@ -146,10 +146,10 @@ __device__ __forceinline__ void stage_bb16(double* dst, const double* __restrict
 }
 
 template <bool A_K, bool B_K, bool BB = false, int NW = 8, int BNT = 128, bool BB16 = false>
-__global__ void __launch_bounds__(NW * 32, BNT == 64 ? 2 : 1)
+__global__ void __launch_bounds__(NW * 32, BNT <= 64 ? 2 : 1)
 dmma_gemm_kernel(GemmParams<double> p, int64_t tiles_m, int64_t tiles_n) {
   extern __shared__ __align__(16) double sm[];
-  static_assert(BNT == 128 || (BNT == 64 && NW == 8), "tile configurations");
+  static_assert(BNT == 128 || (BNT <= 64 && NW == 8), "tile configurations");
   constexpr int NT = NW * 32;
   constexpr int WN = BNT / 32;                       // warps along N (32 columns each)
   constexpr int WM = NW / WN, TM = 128 / WM / 8;     // warps along M, DMMA row tiles per warp

@@ -476,6 +476,10 @@ static int launch_dmma_cfg(const GemmParams<double>& p, cudaStream_t stream) {
     return bn_env == 128 ? launch_dmma_nw<AK, BK_, BB, 8, 128, true>(p, stream)
                          : launch_dmma_nw<AK, BK_, BB, 8, 64, true>(p, stream);
   const int bn = bn_env ? bn_env : (BB ? 128 : 64);
+  // N <= 32 (the rank-r Tucker products of fp64 tensors): 128 x 32 tiles, no idle columns
+  static const int narrow32 = env_int("SBT_DMMA_N32", 1);
+  if (!BB && narrow32 && bn_env == 0 && nw_env == 0 && p.n <= 32)
+    return launch_dmma_nw<AK, BK_, BB, 8, 32>(p, stream);
   if (bn == 64 && nw_env == 0) return launch_dmma_nw<AK, BK_, BB, 8, 64>(p, stream);
   const int nw = nw_env ? nw_env : ((p.k <= 256 && !BB) ? 16 : 8);
   return nw == 16 ? launch_dmma_nw<AK, BK_, BB, 16>(p, stream)

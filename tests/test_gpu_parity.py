@@ -221,6 +221,34 @@ def test_zero_copies_and_one_launch_per_plan():
         assert _lib.launch_count() == n0 + 1, case.case_id
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_zero_copies_at_bench_size(dtype):
+    """The n = 256 sweep extents (every case, both dtypes): no transposition, no
+    tensor allocation, no growth of the caching allocator, one launch per
+    planned contraction -- the device memory the kernels see is the caller's."""
+    n = 256
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a2 = torch.rand(n * n, generator=g, device="cuda", dtype=dtype)
+    b3 = torch.rand(n ** 3, generator=g, device="cuda", dtype=dtype)
+    c3 = torch.empty(n ** 3, device="cuda", dtype=dtype)
+    for case in enumerate_cases(2, 3):
+        spec = ContractionSpec(case.labels_a, case.labels_b, case.labels_c)
+        la, lb, lc = _packed(spec, dict(m=n, n=n, p=n, k=n))
+        a = DenseTensor(la, a2 if la.size == n * n else b3)
+        b = DenseTensor(lb, a2 if lb.size == n * n else b3)
+        c = DenseTensor(lc, c3)
+        plan = plan_single_mode(spec, la, lb, lc)
+        execute_plan(plan, a, b, 1.0, 0.0, c)      # first call: tensor maps, attributes
+        torch.cuda.synchronize()
+        t0, a0, n0 = L.transposition_count(), L.allocation_count(), _lib.launch_count()
+        mem0 = torch.cuda.memory_allocated()
+        execute_plan(plan, a, b, 1.0, 0.0, c)
+        torch.cuda.synchronize()
+        assert (L.transposition_count(), L.allocation_count()) == (t0, a0), case.case_id
+        assert torch.cuda.memory_allocated() == mem0, case.case_id
+        assert _lib.launch_count() == n0 + 1, case.case_id
+
+
 def test_nested_batching_single_launch():
     rng = np.random.default_rng(4)
     spec = ContractionSpec(tuple("mkp"), tuple("nkq"), tuple("mnpq"))

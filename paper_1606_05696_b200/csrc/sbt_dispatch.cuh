@@ -323,6 +323,17 @@ static int launch_pair_single_t(const PairPlan& pl, cudaStream_t stream) {
     if (epib4 && ps.pr[0].nkb <= 4 && ps.pr[0].f.cmode != 0)
       return launch_pair_set<1, SPLIT, BB, BNT, 32, 4>(ps, stream, name);
   }
+  if constexpr (BB) {   // A/B: 16-deep K-blocks for the batch-blocked tiles
+    static const int bb_kb = env_int("SBT_TC_BB_KB", 32);
+    if (bb_kb == 16) {
+      tf32tma::ProblemSet<1> ps16;
+      if (!fill_problem<BB, BNT, 16>(pl, &ps16.pr[0])) return 0;
+      ps16.pr[0].tile_begin = 0;
+      ps16.n = 1;
+      ps16.total = ps.total;
+      return launch_pair_set<1, SPLIT, BB, BNT, 16>(ps16, stream, name);
+    }
+  }
   return launch_pair_set<1, SPLIT, BB, BNT>(ps, stream, name);
 }
 
@@ -372,9 +383,16 @@ struct GroupLaunch {
       int n = 0;
       int64_t total = 0;
       int members[kMaxGroup];
+      static const int bb_kb = BB ? env_int("SBT_TC_BB_KB", 32) : 32;
       for (int i = 0; i < nb; ++i) {
         const PairPlan& pl = plans[idx[base + i]];
-        if (!fill_problem<BB, BNT, 32>(pl, &ps.pr[n])) continue;  // caller relaunches singly
+        bool filled;
+        if constexpr (BB)
+          filled = bb_kb == 16 ? fill_problem<BB, BNT, 16>(pl, &ps.pr[n])
+                               : fill_problem<BB, BNT, 32>(pl, &ps.pr[n]);
+        else
+          filled = fill_problem<BB, BNT, 32>(pl, &ps.pr[n]);
+        if (!filled) continue;  // caller relaunches singly
         ps.pr[n].tile_begin = total;
         total += ps.pr[n].tiles_m * ps.pr[n].tiles_n * ps.pr[n].nbatch *
                  ((ps.pr[n].f.fm == 2 || ps.pr[n].f.fn == 2) ? 1 : pl.p.batch2);
@@ -383,7 +401,16 @@ struct GroupLaunch {
       if (n == 0) continue;
       ps.n = n;
       ps.total = total;
-      rc = launch_pair_set<kMaxGroup, SPLIT, BB, BNT>(ps, stream, pair_name(BB, SPLIT, BNT, false, true));
+      if constexpr (BB) {
+        rc = bb_kb == 16
+                 ? launch_pair_set<kMaxGroup, SPLIT, BB, BNT, 16>(
+                       ps, stream, pair_name(BB, SPLIT, BNT, false, true))
+                 : launch_pair_set<kMaxGroup, SPLIT, BB, BNT>(
+                       ps, stream, pair_name(BB, SPLIT, BNT, false, true));
+      } else {
+        rc = launch_pair_set<kMaxGroup, SPLIT, BB, BNT>(ps, stream,
+                                                        pair_name(BB, SPLIT, BNT, false, true));
+      }
       if (rc >= 0)
         for (int i = 0; i < n; ++i) launched[members[i]] = true;
     }

@@ -786,6 +786,36 @@ def test_hooi_sharded_device_ops_single_rank_equals_hooi():
         dist.destroy_process_group()
 
 
+def test_hooi_iteration_graph_runs_only_library_kernels():
+    """The captured HOOI iteration (device-finished factor updates) launches
+    library kernels only: no PyTorch elementwise / reduction / copy kernels
+    between the contractions, the factor updates and the status kernel."""
+    from torch.profiler import ProfilerActivity, profile
+    from paper_1606_05696_b200 import tucker as tk
+    rng = np.random.default_rng(41)
+    dims, ranks = (160, 144, 128), (8, 8, 8)
+    core = rng.standard_normal(ranks)
+    us = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    full = np.einsum("abc,ia,jb,kc->ijk", core, *us) + 1e-3 * rng.standard_normal(dims)
+    t = DenseTensor.from_array(full, dtype="float32")
+    tk.clear_graph_cache()
+    sbt.hooi(t, ranks, max_iters=5, tol=-1.0)
+    cached = tk._IterationGraph._cache
+    assert cached is not None, "the iteration graph was not captured"
+    graph = cached[1]
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        graph.graphs[graph.cur].replay()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events()
+             if e.device_type == torch.autograd.DeviceType.CUDA and "Memcpy" not in e.name
+             and "Memset" not in e.name]
+    assert names, "no kernels recorded"
+    foreign = [n for n in names if "sbt::" not in n]
+    assert not foreign, foreign
+    tk.clear_graph_cache()
+
+
 def test_hooi_device_ritz_equals_host_path():
     """HOOI with the device-finished sweeps (one host sync per iteration)
     gives the host-driven path's fits and factors, fp32 and fp64."""
